@@ -1,0 +1,153 @@
+/*
+ * pnrte_b200 — C ABI of the B200 (sm_100a) P_N solve path.
+ *
+ * Drop-in boundary for the reference's runtime functions (pnrte):
+ *   assemble(program, spec)            pkg/src/pnrte/solver.py:96      -> pn_create + pn_set_field + pn_setup
+ *   solve_normal_cg(system, tol, max_iter, primal_tol, jacobi, x0)
+ *                                      pkg/src/pnrte/solver.py:189-190 -> pn_solve
+ *   A @ x, A.T @ x (csr_matvec)        pkg/src/pnrte/solver.py:209,226-227,232,239 -> pn_apply
+ *   unstagger(u, program, res)         pkg/src/pnrte/solver.py:275     -> pn_unstagger
+ *   SparseSystem.A / .Q (debug parity) pkg/src/pnrte/solver.py:182-186 -> pn_export_diag_rhs
+ *   A.multiply(A).sum(axis=0)          pkg/src/pnrte/solver.py:219     -> pn_jacobi_diag
+ * The reference has no formal plugin ABI; its Python entry points are the
+ * boundary.  The Python mirror in paper_1807_00410_b200/solver.py
+ * binds these symbols with ctypes (INTEGRATION.md shows the binding).
+ *
+ * Conventions
+ *  - Plain pointers and sizes, no torch types.  Unless a name says _host,
+ *    vector pointers are DEVICE pointers on the context's device, stream
+ *    ordered on the `stream` argument (a cudaStream_t, NULL = legacy default).
+ *  - Vectors use the reference layout: index (i + nx*(j + ny*k))*U + comp,
+ *    comp = l(l+1)+m, over the context's local z-slab [z0, z0+nz_local).
+ *  - Every call returns PN_OK or an error code; pn_last_error() gives the
+ *    message.  Non-convergence is NOT an error (report.converged), exactly
+ *    like the reference (solver.py:247-250).
+ *  - A context is single-stream and not thread safe; use one per GPU/rank.
+ */
+#ifndef PNRTE_B200_H
+#define PNRTE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PN_OK 0
+#define PN_ERR_INVALID 1      /* ValueError in the reference (e.g. tol <= 0, solver.py:200-201) */
+#define PN_ERR_CUDA 2
+#define PN_ERR_UNSUPPORTED 3  /* program outside the matrix-free P_N form */
+#define PN_ERR_NCCL 4
+#define PN_ERR_NOMEM 5
+
+typedef struct pn_context pn_context;
+
+/* Flat stencil tables (paper_1807_00410_b200/program.py:pack_tables), copied
+ * at create.  a_* = rows of A in ascending column order, t_* = rows of A^T in
+ * ascending column order, dir codes 0 same voxel, 1/2 -x/+x, 3/4 -y/+y, 5/6 -z/+z.
+ * Term programs evaluate diag/RHS coefficients in expression-tree order. */
+typedef struct {
+    int32_t N, U;
+    int32_t nx, ny, nz;          /* global grid */
+    int32_t z0, nz_local;        /* this context's z-slab */
+    double h;
+    int32_t device;
+    int32_t n_fields;            /* sigma_t, sigma_s, p_0..p_N, Q by comp */
+    const int32_t *par;          /* [U] staggered parity bits x|y<<1|z<<2 */
+    const double *lam;           /* [U] lambda_l of each comp */
+    const int32_t *lidx;         /* [U] l of each comp */
+    int32_t n_a, n_t, n_terms;
+    const int32_t *a_ptr, *a_tgt, *a_dir, *a_diag; const double *a_w;
+    const int32_t *t_ptr, *t_src, *t_dir, *t_diag; const double *t_w;
+    const int32_t *d_ptr, *r_ptr, *term_hascoef, *term_nf, *term_f, *term_site;
+    const double *term_coef;
+    int32_t canonical_diag;      /* 1: diag = avg(st) - lam*p*avg(ss) form (program.canonical_diag) */
+    /* multi-GPU: NCCL unique id bytes (128) or NULL for a single GPU */
+    const void *nccl_id;
+    int32_t rank, world;
+} pn_desc;
+
+int pn_create(const pn_desc *desc, pn_context **out);
+int pn_destroy(pn_context *ctx);
+const char *pn_last_error(void);
+
+/* Field slot s (order of desc): kind 0 = absent (zero), 1 = uniform scalar,
+ * 2 = array.  Arrays are the reference's [i,j,k] C-order global field
+ * (z fastest) in DEVICE memory; the context transposes its slab (+1 plane).
+ * Fields are consumed by pn_setup and may be freed afterwards. */
+int pn_set_field(pn_context *ctx, int32_t slot, int32_t kind, double scalar,
+                 const double *data, void *stream);
+
+/* Evaluate diagonal (when needed) and RHS Q from the fields (assemble()). */
+int pn_setup(pn_context *ctx, void *stream);
+
+/* Copy the assembled diagonal and RHS into caller buffers (parity/debug). */
+int pn_export_diag_rhs(pn_context *ctx, double *diag, double *rhs, void *stream);
+
+/* y = A x (transpose = 0) or A^T x (transpose = 1).
+ * mode 0 = fast (B200 kernel), 1 = faithful (scipy csr_matvec order, no FMA). */
+int pn_apply(pn_context *ctx, int32_t transpose, int32_t mode, const double *x, double *y, void *stream);
+
+/* colsum(A o A) with 0 kept (the reference replaces 0 by 1 afterwards). */
+int pn_jacobi_diag(pn_context *ctx, double *out, void *stream);
+
+typedef struct {
+    double tol;                  /* > 0 */
+    int64_t max_iter;
+    double primal_tol;           /* < 0 means None */
+    int32_t jacobi;
+    int32_t mode;                /* 0 fast, 1 faithful */
+    int32_t blas_threads;        /* faithful: OpenBLAS thread count to emulate */
+    int32_t blas_kernel;         /* faithful: 0 SkylakeX, 1 Haswell */
+    int32_t check_every;         /* host polls the device stop flag every k iterations (0 = auto) */
+} pn_solve_opts;
+
+typedef struct {
+    int64_t iterations;
+    int32_t converged;
+    double normal_residual;      /* ||A^T(Ax-b)|| / ||A^T b|| */
+    double primal_residual;      /* ||Ax-b|| / ||b|| */
+    double wall_time;            /* seconds, device events around the solve */
+} pn_report;
+
+/* CGNR (solve_normal_cg).  b = NULL uses the assembled RHS.  x0 may be NULL.
+ * x is written (local slab).  Histories are HOST buffers of hist_cap entries
+ * (may be NULL).  Synchronises the stream before returning the report. */
+int pn_solve(pn_context *ctx, const pn_solve_opts *opts, const double *b, const double *x0,
+             double *x, pn_report *report, double *normal_hist, double *primal_hist,
+             int64_t hist_cap, void *stream);
+
+/* Collocated coefficients (*res, U) C-order for the local slab (unstagger()).
+ * Reads the k-1 plane of z-staggered comps from the lower neighbour on
+ * multi-GPU.  out: [nx][ny][nz_local][U]. */
+int pn_unstagger(pn_context *ctx, const double *u, double *out, void *stream);
+
+/* Host-buffer composite (e2e): host fields already set, host x out. */
+int pn_solve_host(pn_context *ctx, const pn_solve_opts *opts, double *x_host,
+                  pn_report *report, double *normal_hist, double *primal_hist, int64_t hist_cap);
+
+/* Number of fast-path kernels launched by this context since creation. */
+int64_t pn_kernel_launches(pn_context *ctx);
+
+/* NCCL unique id (128 bytes) for multi-GPU creation (rank 0 calls it). */
+int pn_nccl_unique_id(void *out128);
+
+/* Loopback slab group: several contexts on ONE device whose halos and
+ * partial sums are exchanged by device copies instead of NCCL (tests of the
+ * slab decomposition on one GPU).  Contexts must be created with world > 1,
+ * nccl_id = NULL, ranks 0..n-1 in order. */
+int pn_group_solve(pn_context **ctxs, int32_t n, const pn_solve_opts *opts, double **x,
+                   pn_report *report, double *normal_hist, double *primal_hist, int64_t hist_cap,
+                   void *stream);
+int pn_group_apply(pn_context **ctxs, int32_t n, int32_t transpose, int32_t mode,
+                   const double **x, double **y, void *stream);
+
+/* Kernel-level timing hooks for bench.py: run `reps` back-to-back fast
+ * applies (or fused CG iterations, what = 1) on internal buffers and return
+ * the average device time per launch in milliseconds. */
+int pn_bench(pn_context *ctx, int32_t what, int32_t reps, double *ms_per, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,179 @@
+// Internal types of the B200 P_N runtime (not part of the C ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string>
+#include <vector>
+
+#include "../../include/pnrte_b200.h"
+
+namespace pn {
+
+// ---------------------------------------------------------------- errors --
+void set_error(const std::string &msg);
+#define PN_CUDA(call)                                                              \
+    do {                                                                           \
+        cudaError_t e_ = (call);                                                   \
+        if (e_ != cudaSuccess) {                                                   \
+            ::pn::set_error(std::string(#call) + ": " + cudaGetErrorString(e_));   \
+            return PN_ERR_CUDA;                                                    \
+        }                                                                          \
+    } while (0)
+#define PN_TRY(call)            \
+    do {                        \
+        int s_ = (call);        \
+        if (s_ != PN_OK) return s_; \
+    } while (0)
+
+// --------------------------------------------------------- device tables --
+// Everything a kernel needs to know about the operator, passed by value.
+struct Geo {
+    int U, nx, ny, nz;      // global grid
+    int z0, nzl;            // slab
+    long long plane;        // doubles per z-plane of a vector = nx*ny*U
+    long long pvox;         // voxels per plane = nx*ny
+};
+
+struct Tables {
+    const int *par;         // [U] parity bits
+    const double *lamp;     // [U] lambda_l * p_l (uniform phase fields)
+    const int *a_ptr, *a_tgt, *a_dir, *a_diag; const double *a_w;
+    const int *t_ptr, *t_src, *t_dir, *t_diag; const double *t_w;
+    const int *d_ptr, *r_ptr, *hascoef, *nf, *tf, *tsite; const double *tcoef;
+    int n_a, n_t;
+};
+
+constexpr int MAX_FIELDS = 2 + 8 + 64 + 8;
+struct Fields {
+    int n;
+    int kind[MAX_FIELDS];
+    double scalar[MAX_FIELDS];
+    const double *data[MAX_FIELDS];   // slab arrays, (nzl+1) planes, x fastest
+};
+
+// device-resident solver scalars (one struct, updated by scalar kernels)
+struct State {
+    double rho, alpha, beta;
+    double norm_b, norm_atb;
+    double ww, zz, zzt, rr;
+    double tol, primal_tol;
+    long long it;           // completed iterations
+    long long max_iter;
+    int done;               // stop flag: all iteration kernels become no-ops
+    int converged;
+    int zero_ww;
+};
+
+// number of fast-reduction partial slots per (plane, block)
+constexpr int RED_SLOTS = 4;   // 0: ww / zzt, 1: zz, 2: rr, 3: spare
+
+struct Comm;   // halo + partial exchange (NCCL or loopback)
+
+// ------------------------------------------------------------- context --
+struct Buf {
+    double *alloc = nullptr;  // includes one halo plane each side
+    double *p = nullptr;      // interior base (plane 0 of the slab)
+};
+
+}  // namespace pn
+
+struct pn_context {
+    int N = 0, U = 0;
+    pn::Geo g{};
+    double h = 0;
+    int device = 0;
+    int rank = 0, world = 1;
+    int canonical_diag = 0;
+    int uniform_phase = 1;
+    int n_fields = 0;
+
+    // tables (device)
+    std::vector<void *> dev_allocs;
+    pn::Tables tb{};
+    std::vector<int> h_par, h_lidx;
+    std::vector<double> h_lam;
+
+    // fields
+    pn::Fields f{};
+    std::vector<double *> field_alloc;
+
+    // assembled operator state
+    double *diag = nullptr;       // [R_l] (faithful / non-canonical path)
+    pn::Buf b;                    // RHS
+    bool setup_done = false;
+    bool diag_ready = false;
+
+    // Krylov vectors (padded with z-halo planes)
+    pn::Buf x, r, p, z, zt, w, tmp, minv;
+    bool vecs_ready = false;
+
+    // reductions
+    int red_bx = 0;               // blocks per plane for reductions
+    double *partials = nullptr;   // [nz * red_bx * RED_SLOTS] global layout
+    double *ddot_chunks = nullptr;// faithful ddot chunk results [4][64]
+    pn::State *state = nullptr;   // device
+    pn::State *h_state = nullptr; // pinned host mirror
+    double *hist_n = nullptr, *hist_p = nullptr;  // device histories
+    long long hist_len = 0;
+
+    // comm
+    pn::Comm *comm = nullptr;
+    void *nccl = nullptr;         // ncclComm_t
+
+    long long launches = 0;
+
+    // segmented fast path (pn_seg.cu)
+    void *seg = nullptr;
+    pn::Buf bs;                   // RHS in the solve layout
+    std::vector<double> h_aw, h_tw;
+
+    long long R_l() const { return (long long)g.nzl * g.plane; }
+    long long nvox_l() const { return (long long)g.nzl * g.pvox; }
+};
+
+namespace pn {
+
+// kernels (pn_kernels.cu)
+int launch_fill(double *p, long long n, double v, cudaStream_t s);
+int launch_field_slab(pn_context *c, int slot, const double *src, double *dst, cudaStream_t s);
+int launch_setup(pn_context *c, bool want_diag, cudaStream_t s);
+int launch_apply_table(pn_context *c, int trans, int faithful, int squared, const double *x, double *y, int red,
+                       const double *minv, double *zt, cudaStream_t s, bool gated);
+int launch_apply_faithful(pn_context *c, int trans, int squared, const double *x, double *y,
+                          cudaStream_t s, bool gated = false);
+int launch_xr(pn_context *c, cudaStream_t s);
+int launch_pupd(pn_context *c, const double *zt, cudaStream_t s);
+int launch_dot(pn_context *c, const double *a, const double *b, int slot, cudaStream_t s, bool gated = false);
+int launch_ddot_emul(pn_context *c, const double *a, const double *b, long long n, int slot, int threads,
+                     int kernel, cudaStream_t s, bool gated = false);
+int launch_unstagger(pn_context *c, const double *u, double *out, cudaStream_t s);
+
+// elementwise ops, see pn_kernels.cu for the op codes
+int launch_vec(pn_context *c, int op, double *y, const double *a, const double *b, cudaStream_t s,
+               bool gated = false);
+
+enum VecOp {
+    V_COPY = 0,        // y = a
+    V_ZERO,            // y = 0
+    V_SUB,             // y = a - b
+    V_MUL,             // y = a * b
+    V_RECIP_DIAG,      // y = 1/(a == 0 ? 1 : a)
+    V_AXPY_ALPHA,      // y = y + (alpha * a)           (numpy: x += alpha*p)
+    V_AXMY_ALPHA,      // y = y - (alpha * a)           (numpy: r -= alpha*w)
+    V_P_UPDATE,        // y = a + (beta * y)            (numpy: p = zt + beta*p)
+    V_FILL_ONE,        // y = 1
+};
+
+// reduction slots: 0 generic / ww, 1 zz, 2 z.zt, 3 rr (fast partials and
+// faithful ddot chunks use the same numbering)
+enum Scalar {
+    S_NORMB = 0,       // norm_b = sqrt(slot 0)
+    S_NORMATB,         // norm_atb = sqrt(slot 0)
+    S_RHO,             // rho = slot 2
+    S_ALPHA,           // ww = slot 0 -> alpha (or stop without counting)
+    S_BETA,            // zz, zzt, rr -> history, stop test, beta, rho
+    S_FINAL,           // zz = slot 0, rr = slot 3 (true residuals)
+};
+int launch_scalar(pn_context *c, int which, int faithful, int blas_threads, cudaStream_t s);
+
+}  // namespace pn

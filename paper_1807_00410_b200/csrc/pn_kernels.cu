@@ -1,0 +1,639 @@
+// Generic sm_100a kernels of the P_N solve path: field upload, assembly of
+// the diagonal / RHS, the faithful (scipy-order) operator, the table-driven
+// fast operator for grids the segmented kernel does not cover, elementwise
+// CG updates, deterministic reductions, the OpenBLAS ddot emulation used by
+// the faithful mode, the solver scalar steps and unstagger.
+//
+// Reference behaviour mirrored (pkg/src/pnrte/):
+//   assemble            solver.py:96-186   (k_setup: diag/RHS in tree order, pinned rows)
+//   csr_matvec          solver.py:209-255  (k_apply_table: ascending column order, no FMA)
+//   solve_normal_cg     solver.py:189-257  (k_vec + k_scalar)
+//   unstagger           solver.py:275-296  (k_unstagger)
+// This file is compiled with -fmad=false: faithful arithmetic must never be
+// contracted into FMAs (numpy / sparsetools do mul then add).  Kernels that
+// may use FMA live in pn_seg.cu.
+#include <cuda_runtime.h>
+#include <math.h>
+
+#include "pn_internal.cuh"
+
+namespace pn {
+
+__device__ __forceinline__ bool stopped(const State *st) { return *(volatile const int *)&st->done != 0; }
+
+// ------------------------------------------------------------ field slab --
+// src: [i][j][k] C-order global field.  dst: planes kl = 0..nzl (global
+// k = min(z0+kl, nz-1), the +1 plane is the edge-replicated sample of
+// solver.py:62-64), x fastest.  32x32 smem transpose per j.
+__global__ void k_field_slab(const double *__restrict__ src, double *__restrict__ dst, int nx, int ny, int nz,
+                             int z0, int nplanes) {
+    __shared__ double tile[32][33];
+    const int j = blockIdx.z;
+    const int i0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
+    for (int r = threadIdx.y; r < 32; r += 8) {
+        int i = i0 + r, kl = k0 + threadIdx.x;
+        if (i < nx && kl < nplanes) {
+            int kg = min(z0 + kl, nz - 1);
+            tile[r][threadIdx.x] = src[((long long)i * ny + j) * nz + kg];
+        }
+    }
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += 8) {
+        int kl = k0 + r, i = i0 + threadIdx.x;
+        if (i < nx && kl < nplanes) dst[((long long)kl * ny + j) * nx + i] = tile[threadIdx.x][r];
+    }
+}
+
+int launch_field_slab(pn_context *c, int slot, const double *src, double *dst, cudaStream_t s) {
+    const Geo &g = c->g;
+    int nplanes = g.nzl + 1;
+    dim3 grid((g.nx + 31) / 32, (nplanes + 31) / 32, g.ny), block(32, 8);
+    k_field_slab<<<grid, block, 0, s>>>(src, dst, g.nx, g.ny, g.nz, g.z0, nplanes);
+    PN_CUDA(cudaGetLastError());
+    return PN_OK;
+}
+
+__global__ void k_fill(double *p, long long n, double v) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        p[i] = v;
+}
+
+int launch_fill(double *p, long long n, double v, cudaStream_t s) {
+    k_fill<<<1184, 256, 0, s>>>(p, n, v);
+    PN_CUDA(cudaGetLastError());
+    return PN_OK;
+}
+
+// ---------------------------------------------------------------- setup --
+__device__ __forceinline__ double fsample(const Fields &F, const Geo &g, int slot, int i, int j, int kl, int site) {
+    int kd = F.kind[slot];
+    if (kd == 0) return 0.0;
+    if (kd == 1) return F.scalar[slot];
+    int ii = min(i + (site & 1), g.nx - 1);
+    int jj = min(j + ((site >> 1) & 1), g.ny - 1);
+    int kk = kl + ((site >> 2) & 1);   // plane nzl exists (clamped at upload)
+    return F.data[slot][(long long)kk * g.pvox + (long long)jj * g.nx + ii];
+}
+
+__device__ double eval_terms(const Tables &T, const Fields &F, const Geo &g, int t0, int t1, int i, int j, int kl) {
+    double acc = 0.0;
+    for (int t = t0; t < t1; ++t) {
+        int nf = T.nf[t], f = 0;
+        double v;
+        if (T.hascoef[t]) v = T.tcoef[t];
+        else { v = fsample(F, g, T.tf[2 * t], i, j, kl, T.tsite[2 * t]); f = 1; }
+        for (; f < nf; ++f) v = __dmul_rn(v, fsample(F, g, T.tf[2 * t + f], i, j, kl, T.tsite[2 * t + f]));
+        acc = (t == t0) ? v : __dadd_rn(acc, v);
+    }
+    return acc;
+}
+
+__device__ __forceinline__ int boundary_bits(const Geo &g, int i, int j, int kg) {
+    return (i == g.nx - 1) | ((j == g.ny - 1) << 1) | ((kg == g.nz - 1) << 2);
+}
+
+// one thread per (local voxel, comp): diag (optional) and RHS (solver.py:136-181)
+__global__ void k_setup(Tables T, Fields F, Geo g, double *diag, double *rhs) {
+    long long row = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    long long R = (long long)g.nzl * g.plane;
+    if (row >= R) return;
+    long long v = row / g.U;
+    int c = (int)(row - v * g.U);
+    int i = (int)(v % g.nx);
+    int j = (int)((v / g.nx) % g.ny);
+    int kl = (int)(v / g.pvox);
+    int bb = boundary_bits(g, i, j, g.z0 + kl);
+    if (diag) diag[row] = eval_terms(T, F, g, T.d_ptr[c], T.d_ptr[c + 1], i, j, kl);
+    double r = 0.0;
+    if (T.r_ptr[c + 1] > T.r_ptr[c]) r = -eval_terms(T, F, g, T.r_ptr[c], T.r_ptr[c + 1], i, j, kl);
+    rhs[row] = (T.par[c] & bb) ? 0.0 : r;
+}
+
+int launch_setup(pn_context *c, bool want_diag, cudaStream_t s) {
+    long long R = c->R_l();
+    int bs = 256;
+    long long nb = (R + bs - 1) / bs;
+    k_setup<<<(unsigned)nb, bs, 0, s>>>(c->tb, c->f, c->g, want_diag ? c->diag : nullptr, c->b.p);
+    PN_CUDA(cudaGetLastError());
+    c->launches++;
+    return PN_OK;
+}
+
+// ------------------------------------------------------ table operator --
+__constant__ int c_dx[7] = {0, -1, 1, 0, 0, 0, 0};
+__constant__ int c_dy[7] = {0, 0, 0, -1, 1, 0, 0};
+__constant__ int c_dz[7] = {0, 0, 0, 0, 0, -1, 1};
+
+// Shared-memory copy of one table direction (rows in ascending column order).
+struct SmemTab {
+    int *ptr, *oth, *dir, *isd;
+    double *w;
+};
+
+// Block reduction of up to 3 per-thread values into partials (fixed tree).
+template <int NV>
+__device__ __forceinline__ void block_partials(double (&v)[NV], double *partials, const int *slots, long long slot_stride,
+                                               long long idx) {
+    __shared__ double red[NV][32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+        double a = v[q];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) a = __dadd_rn(a, __shfl_down_sync(0xffffffffu, a, o));
+        if (lane == 0) red[q][wid] = a;
+    }
+    __syncthreads();
+    if (wid == 0) {
+#pragma unroll
+        for (int q = 0; q < NV; ++q) {
+            double a = lane < nw ? red[q][lane] : 0.0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) a = __dadd_rn(a, __shfl_down_sync(0xffffffffu, a, o));
+            if (lane == 0) partials[slots[q] * slot_stride + idx] = a;
+        }
+    }
+}
+
+// red: 0 none, 1 = sum y^2 -> slot 0, 2 = z/zt: sum z*zt -> slot 2, sum z^2 -> slot 1
+// faithful: sequential mul-then-add in table order starting from 0 (scipy
+// csr_matvec); otherwise FMA and the recomputed or stored diagonal.
+template <bool FAITHFUL, bool RECOMPUTE_DIAG>
+__global__ void __launch_bounds__(256) k_apply_table(Tables T, Fields F, Geo g, int trans, int squared,
+                                                     const double *__restrict__ x, double *__restrict__ y,
+                                                     const double *__restrict__ diag, int red, const double *minv,
+                                                     double *zt, double *partials, long long slot_stride, int rb,
+                                                     const State *st) {
+    if (st && stopped(st)) return;
+    extern __shared__ unsigned char smem_raw[];
+    const int U = g.U;
+    const int ne = trans ? T.n_t : T.n_a;
+    double *sw = (double *)smem_raw;
+    int *sptr = (int *)(sw + ne);
+    int *soth = sptr + U + 1, *sdir = soth + ne, *sisd = sdir + ne;
+    int *spar = sisd + ne;
+    double *slamp = (double *)(((uintptr_t)(spar + U) + 15) & ~(uintptr_t)15);
+    {
+        const int *p_ = trans ? T.t_ptr : T.a_ptr;
+        const int *o_ = trans ? T.t_src : T.a_tgt;
+        const int *d_ = trans ? T.t_dir : T.a_dir;
+        const int *i_ = trans ? T.t_diag : T.a_diag;
+        const double *w_ = trans ? T.t_w : T.a_w;
+        for (int e = threadIdx.x; e < ne; e += blockDim.x) {
+            sw[e] = w_[e]; soth[e] = o_[e]; sdir[e] = d_[e]; sisd[e] = i_[e];
+        }
+        for (int e = threadIdx.x; e <= U; e += blockDim.x) sptr[e] = p_[e];
+        for (int e = threadIdx.x; e < U; e += blockDim.x) { spar[e] = T.par[e]; slamp[e] = T.lamp[e]; }
+    }
+    __syncthreads();
+    const int kl = blockIdx.y;
+    const long long chunk = (g.plane + rb - 1) / rb;
+    const long long r0 = (long long)blockIdx.x * chunk;
+    const long long r1 = min(g.plane, r0 + chunk);
+    double acc_r[2] = {0.0, 0.0};
+    const int kg = g.z0 + kl;
+    for (long long rp = r0 + threadIdx.x; rp < r1; rp += blockDim.x) {
+        const long long row = (long long)kl * g.plane + rp;
+        const long long vp = rp / U;
+        const int c = (int)(rp - vp * U);
+        const int i = (int)(vp % g.nx), j = (int)(vp / g.nx);
+        const int bb = boundary_bits(g, i, j, kg);
+        const bool pinned_c = (spar[c] & bb) != 0;
+        double sum = 0.0;
+        for (int e = sptr[c]; e < sptr[c + 1]; ++e) {
+            const int o = soth[e];
+            double a, xv;
+            if (sisd[e]) {
+                if (RECOMPUTE_DIAG) {
+                    // avg over the staggered site set, then diag = avg_t - lamp*avg_s
+                    const int pc = spar[c];
+                    double st_ = 0.0, ss_ = 0.0;
+                    int n = 0;
+                    for (int s = 0; s < 8; ++s) {
+                        if (s & ~pc) continue;
+                        st_ += fsample(F, g, 0, i, j, kl, s);
+                        ss_ += fsample(F, g, 1, i, j, kl, s);
+                        ++n;
+                    }
+                    const double inv = 1.0 / n;
+                    a = st_ * inv - slamp[c] * (ss_ * inv);
+                } else {
+                    a = diag[row];
+                }
+                xv = x[row];
+            } else {
+                const int d = sdir[e];
+                const int ii = i + c_dx[d], jj = j + c_dy[d], kk = kg + c_dz[d];
+                if (pinned_c || ii < 0 || jj < 0 || kk < 0 || ii >= g.nx || jj >= g.ny || kk >= g.nz) continue;
+                const int nbb = (ii == g.nx - 1) | ((jj == g.ny - 1) << 1) | ((kk == g.nz - 1) << 2);
+                if (spar[o] & nbb) continue;
+                a = sw[e];
+                xv = x[((long long)(kk - g.z0) * g.pvox + (long long)jj * g.nx + ii) * U + o];
+            }
+            if (FAITHFUL) {
+                if (squared) a = __dmul_rn(a, a);
+                sum = __dadd_rn(sum, __dmul_rn(a, xv));
+            } else {
+                sum = fma(a, xv, sum);
+            }
+        }
+        y[row] = sum;
+        if (red == 1) {
+            acc_r[0] = fma(sum, sum, acc_r[0]);
+        } else if (red == 2) {
+            double t = minv ? sum * minv[row] : sum;
+            if (zt) zt[row] = t;
+            acc_r[0] = fma(sum, t, acc_r[0]);
+            acc_r[1] = fma(sum, sum, acc_r[1]);
+        }
+    }
+    if (red) {
+        const long long idx = (long long)kg * rb + blockIdx.x;
+        if (red == 1) {
+            double v[1] = {acc_r[0]};
+            const int sl[1] = {0};
+            block_partials<1>(v, partials, sl, slot_stride, idx);
+        } else {
+            double v[2] = {acc_r[0], acc_r[1]};
+            const int sl[2] = {2, 1};
+            block_partials<2>(v, partials, sl, slot_stride, idx);
+        }
+    }
+}
+
+static size_t table_smem(const pn_context *c, int trans) {
+    int ne = trans ? c->tb.n_t : c->tb.n_a;
+    size_t b = (size_t)ne * 8 + (size_t)(c->U + 1) * 4 + (size_t)ne * 12 + (size_t)c->U * 4;
+    b = (b + 15) & ~(size_t)15;
+    return b + (size_t)c->U * 8 + 16;
+}
+
+static long long slot_stride(const pn_context *c) { return (long long)c->g.nz * c->red_bx; }
+
+int launch_apply_table(pn_context *c, int trans, int faithful, int squared, const double *x, double *y, int red,
+                       const double *minv, double *zt, cudaStream_t s, bool gated) {
+    dim3 grid(c->red_bx, c->g.nzl);
+    size_t sm = table_smem(c, trans);
+    const State *st = gated ? c->state : nullptr;
+    bool recompute = !faithful && c->canonical_diag && c->uniform_phase && c->diag == nullptr;
+    if (faithful) {
+        k_apply_table<true, false><<<grid, 256, sm, s>>>(c->tb, c->f, c->g, trans, squared, x, y, c->diag, red, minv,
+                                                         zt, c->partials, slot_stride(c), c->red_bx, st);
+    } else if (recompute) {
+        k_apply_table<false, true><<<grid, 256, sm, s>>>(c->tb, c->f, c->g, trans, 0, x, y, c->diag, red, minv, zt,
+                                                         c->partials, slot_stride(c), c->red_bx, st);
+    } else {
+        k_apply_table<false, false><<<grid, 256, sm, s>>>(c->tb, c->f, c->g, trans, 0, x, y, c->diag, red, minv, zt,
+                                                          c->partials, slot_stride(c), c->red_bx, st);
+    }
+    PN_CUDA(cudaGetLastError());
+    c->launches++;
+    return PN_OK;
+}
+
+int launch_apply_faithful(pn_context *c, int trans, int squared, const double *x, double *y, cudaStream_t s,
+                          bool gated) {
+    return launch_apply_table(c, trans, 1, squared, x, y, 0, nullptr, nullptr, s, gated);
+}
+
+// ----------------------------------------------------------- vector ops --
+__global__ void __launch_bounds__(256) k_vec(int op, Geo g, double *y, const double *a, const double *b, State *st,
+                                             double *partials, long long slot_stride, int rb, int gated) {
+    if (gated && stopped(st)) return;
+    const int kl = blockIdx.y;
+    const long long chunk = (g.plane + rb - 1) / rb;
+    const long long r0 = (long long)blockIdx.x * chunk;
+    const long long r1 = min(g.plane, r0 + chunk);
+    const long long base = (long long)kl * g.plane;
+    const double alpha = st ? st->alpha : 0.0, beta = st ? st->beta : 0.0;
+    for (long long rp = r0 + threadIdx.x; rp < r1; rp += blockDim.x) {
+        const long long i = base + rp;
+        switch (op) {
+            case V_COPY: y[i] = a[i]; break;
+            case V_ZERO: y[i] = 0.0; break;
+            case V_FILL_ONE: y[i] = 1.0; break;
+            case V_SUB: y[i] = __dsub_rn(a[i], b[i]); break;
+            case V_MUL: y[i] = __dmul_rn(a[i], b[i]); break;
+            case V_RECIP_DIAG: { double d = a[i]; y[i] = __ddiv_rn(1.0, d == 0.0 ? 1.0 : d); } break;
+            case V_AXPY_ALPHA: y[i] = __dadd_rn(y[i], __dmul_rn(alpha, a[i])); break;
+            case V_AXMY_ALPHA: y[i] = __dsub_rn(y[i], __dmul_rn(alpha, a[i])); break;
+            case V_P_UPDATE: y[i] = __dadd_rn(a[i], __dmul_rn(beta, y[i])); break;
+        }
+    }
+}
+
+// fast fused x/r update with ||r||^2 partials (slot 3)
+__global__ void __launch_bounds__(256) k_xr(Geo g, double *__restrict__ x, double *__restrict__ r,
+                                            const double *__restrict__ p, const double *__restrict__ w, const State *st,
+                                            double *partials, long long slot_stride, int rb) {
+    if (stopped(st)) return;
+    const int kl = blockIdx.y;
+    const long long chunk = (g.plane + rb - 1) / rb;
+    const long long r0 = (long long)blockIdx.x * chunk;
+    const long long r1 = min(g.plane, r0 + chunk);
+    const long long base = (long long)kl * g.plane;
+    const double alpha = st->alpha;
+    double acc = 0.0;
+    for (long long rp = r0 + threadIdx.x; rp < r1; rp += blockDim.x) {
+        const long long i = base + rp;
+        x[i] = fma(alpha, p[i], x[i]);
+        double rv = fma(-alpha, w[i], r[i]);
+        r[i] = rv;
+        acc = fma(rv, rv, acc);
+    }
+    double v[1] = {acc};
+    const int sl[1] = {3};
+    block_partials<1>(v, partials, sl, slot_stride, (long long)(g.z0 + kl) * rb + blockIdx.x);
+}
+
+// fast p = zt + beta p
+__global__ void __launch_bounds__(256) k_pupd(Geo g, double *__restrict__ p, const double *__restrict__ zt,
+                                              const State *st, int rb) {
+    if (stopped(st)) return;
+    const int kl = blockIdx.y;
+    const long long chunk = (g.plane + rb - 1) / rb;
+    const long long r0 = (long long)blockIdx.x * chunk;
+    const long long r1 = min(g.plane, r0 + chunk);
+    const long long base = (long long)kl * g.plane;
+    const double beta = st->beta;
+    for (long long rp = r0 + threadIdx.x; rp < r1; rp += blockDim.x) {
+        const long long i = base + rp;
+        p[i] = fma(beta, p[i], zt[i]);
+    }
+}
+
+// deterministic dot products into slot (per plane-block partials)
+__global__ void __launch_bounds__(256) k_dot(Geo g, const double *__restrict__ a, const double *__restrict__ b,
+                                             int slot, double *partials, long long slot_stride, int rb,
+                                             const State *st) {
+    if (st && stopped(st)) return;
+    const int kl = blockIdx.y;
+    const long long chunk = (g.plane + rb - 1) / rb;
+    const long long r0 = (long long)blockIdx.x * chunk;
+    const long long r1 = min(g.plane, r0 + chunk);
+    const long long base = (long long)kl * g.plane;
+    double acc = 0.0;
+    for (long long rp = r0 + threadIdx.x; rp < r1; rp += blockDim.x) acc = fma(a[base + rp], b[base + rp], acc);
+    double v[1] = {acc};
+    const int sl[1] = {slot};
+    block_partials<1>(v, partials, sl, slot_stride, (long long)(g.z0 + kl) * rb + blockIdx.x);
+}
+
+int launch_vec(pn_context *c, int op, double *y, const double *a, const double *b, cudaStream_t s, bool gated) {
+    dim3 grid(c->red_bx, c->g.nzl);
+    k_vec<<<grid, 256, 0, s>>>(op, c->g, y, a, b, c->state, c->partials, slot_stride(c), c->red_bx, gated ? 1 : 0);
+    PN_CUDA(cudaGetLastError());
+    c->launches++;
+    return PN_OK;
+}
+
+int launch_xr(pn_context *c, cudaStream_t s) {
+    dim3 grid(c->red_bx, c->g.nzl);
+    k_xr<<<grid, 256, 0, s>>>(c->g, c->x.p, c->r.p, c->p.p, c->w.p, c->state, c->partials, slot_stride(c),
+                              c->red_bx);
+    PN_CUDA(cudaGetLastError());
+    c->launches++;
+    return PN_OK;
+}
+
+int launch_pupd(pn_context *c, const double *zt, cudaStream_t s) {
+    dim3 grid(c->red_bx, c->g.nzl);
+    k_pupd<<<grid, 256, 0, s>>>(c->g, c->p.p, zt, c->state, c->red_bx);
+    PN_CUDA(cudaGetLastError());
+    c->launches++;
+    return PN_OK;
+}
+
+int launch_dot(pn_context *c, const double *a, const double *b, int slot, cudaStream_t s, bool gated) {
+    dim3 grid(c->red_bx, c->g.nzl);
+    k_dot<<<grid, 256, 0, s>>>(c->g, a, b, slot, c->partials, slot_stride(c), c->red_bx, gated ? c->state : nullptr);
+    PN_CUDA(cudaGetLastError());
+    c->launches++;
+    return PN_OK;
+}
+
+// ------------------------------------------------- OpenBLAS ddot emulation --
+// OpenBLAS 0.3.30 ddot (numpy's x @ y and np.linalg.norm):
+// T-way chunking width = ceil(rem/(T-t)) when n > 10000, chunk results
+// summed in order from 0.0.  Per chunk, SkylakeX kernel: 4x8-lane FMA
+// accumulators over 32-blocks, fold hi+lo to 4x4 lanes, 4x4-lane FMA over
+// the 16-block remainder, lanewise ((a0+a1)+a2)+a3, (s0+s2)+(s1+s3), FMA
+// scalar tail.  Haswell kernel: 4x4-lane FMA over 16-blocks, fold to 2 lanes,
+// (h0+h1)+(h2+h3), lane sum, mul-then-add tail.  One warp per chunk.
+__device__ __forceinline__ void chunk_range(long long n, int T, int t, long long &off, long long &width) {
+    long long rem = n;
+    off = 0;
+    width = 0;
+    for (int q = 0; q <= t; ++q) {
+        width = (rem + (T - q) - 1) / (T - q);
+        if (width > rem) width = rem;
+        if (q < t) { off += width; rem -= width; }
+    }
+}
+
+__global__ void k_ddot_emul(const double *__restrict__ x, const double *__restrict__ y, long long n, int T, int kernel,
+                            double *out, const State *st) {
+    if (st && stopped(st)) return;
+    const int lane = threadIdx.x;
+    long long off, w;
+    if (n <= 10000 || T <= 1) { off = 0; w = n; }
+    else chunk_range(n, T, blockIdx.x, off, w);
+    x += off;
+    y += off;
+    double dot = 0.0;
+    if (kernel == 0) {
+        const long long n32 = w & ~31LL, n16 = w & ~15LL;
+        const int q = lane >> 3, l8 = lane & 7;
+        double a8 = 0.0;
+        for (long long i = 0; i < n32; i += 32) a8 = fma(x[i + 8 * q + l8], y[i + 8 * q + l8], a8);
+        // fold to 4 lanes per accumulator: a4[q][l] = a8[q][l] + a8[q][l+4]
+        double hi = __shfl_down_sync(0xffffffffu, a8, 4);
+        double a4 = __dadd_rn(a8, hi);   // valid for l8 < 4
+        if (n32 < n16 && l8 < 4) a4 = fma(x[n32 + 4 * q + l8], y[n32 + 4 * q + l8], a4);
+        // lanewise ((a0+a1)+a2)+a3 over q, lane l8<4 of each q group
+        double a_1 = __shfl_sync(0xffffffffu, a4, 8 + (lane & 3));
+        double a_2 = __shfl_sync(0xffffffffu, a4, 16 + (lane & 3));
+        double a_3 = __shfl_sync(0xffffffffu, a4, 24 + (lane & 3));
+        double s = __dadd_rn(__dadd_rn(__dadd_rn(a4, a_1), a_2), a_3);   // valid at lanes 0..3
+        double s0 = __shfl_sync(0xffffffffu, s, 0), s1 = __shfl_sync(0xffffffffu, s, 1);
+        double s2 = __shfl_sync(0xffffffffu, s, 2), s3 = __shfl_sync(0xffffffffu, s, 3);
+        if (lane == 0) {
+            dot = n16 ? __dadd_rn(__dadd_rn(s0, s2), __dadd_rn(s1, s3)) : 0.0;
+            for (long long i = n16; i < w; ++i) dot = fma(y[i], x[i], dot);
+        }
+    } else {
+        const long long n16 = w & ~15LL;
+        const int q = (lane >> 2) & 3, l4 = lane & 3;
+        double a4 = 0.0;
+        if (lane < 16)
+            for (long long i = 0; i < n16; i += 16) a4 = fma(x[i + 4 * q + l4], y[i + 4 * q + l4], a4);
+        double hi = __shfl_down_sync(0xffffffffu, a4, 2);
+        double h = __dadd_rn(a4, hi);   // valid at l4 < 2
+        double h1 = __shfl_sync(0xffffffffu, h, 4 + (lane & 1));
+        double h2 = __shfl_sync(0xffffffffu, h, 8 + (lane & 1));
+        double h3 = __shfl_sync(0xffffffffu, h, 12 + (lane & 1));
+        double t = __dadd_rn(__dadd_rn(h, h1), __dadd_rn(h2, h3));   // lanes 0,1
+        double t0 = __shfl_sync(0xffffffffu, t, 0), t1 = __shfl_sync(0xffffffffu, t, 1);
+        if (lane == 0) {
+            dot = n16 ? __dadd_rn(t0, t1) : 0.0;
+            for (long long i = n16; i < w; ++i) dot = __dadd_rn(dot, __dmul_rn(y[i], x[i]));
+        }
+    }
+    if (lane == 0) out[blockIdx.x] = dot;
+}
+
+int launch_ddot_emul(pn_context *c, const double *a, const double *b, long long n, int slot, int threads, int kernel,
+                     cudaStream_t s, bool gated) {
+    int nb = (n <= 10000 || threads <= 1) ? 1 : threads;
+    if (nb > 64) { set_error("blas_threads > 64"); return PN_ERR_INVALID; }
+    k_ddot_emul<<<nb, 32, 0, s>>>(a, b, n, threads, kernel, c->ddot_chunks + slot * 64, gated ? c->state : nullptr);
+    PN_CUDA(cudaGetLastError());
+    c->launches++;
+    return PN_OK;
+}
+
+// -------------------------------------------------------- scalar steps --
+// One block: fixed-order sums of the plane-block partials (fast) or the
+// in-order combination of ddot chunks (faithful), then the CGNR scalar logic
+// of solver.py:231-253 on thread 0.
+struct ScalarArgs {
+    const double *partials;
+    long long n_part;            // entries per slot (nz * rb)
+    const double *chunks;
+    int faithful, nchunks;
+    double *hist_n, *hist_p;
+    long long hist_len;
+};
+
+__device__ double sum_slot(const ScalarArgs &a, int slot, double *sh) {
+    const double *p = a.partials + slot * a.n_part;
+    double acc = 0.0;
+    for (long long i = threadIdx.x; i < a.n_part; i += blockDim.x) acc = __dadd_rn(acc, p[i]);
+    sh[threadIdx.x] = acc;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+        if (threadIdx.x < o) sh[threadIdx.x] = __dadd_rn(sh[threadIdx.x], sh[threadIdx.x + o]);
+        __syncthreads();
+    }
+    double r = sh[0];
+    __syncthreads();
+    return r;
+}
+
+__device__ double chunk_sum(const ScalarArgs &a, int slot) {
+    const double *c = a.chunks + slot * 64;
+    if (a.nchunks == 1) return c[0];
+    double d = 0.0;
+    for (int t = 0; t < a.nchunks; ++t) d = __dadd_rn(d, c[t]);
+    return d;
+}
+
+__global__ void __launch_bounds__(256) k_scalar(int which, ScalarArgs a, State *st) {
+    __shared__ double sh[256];
+    if ((which == S_ALPHA || which == S_BETA) && stopped(st)) return;
+    // slots each step consumes: 0 generic / ww, 1 zz, 2 zzt, 3 rr
+    int mask = 0;
+    switch (which) {
+        case S_NORMB: case S_NORMATB: case S_ALPHA: mask = 1; break;
+        case S_RHO: mask = 4; break;
+        case S_BETA: mask = 2 | 4 | 8; break;
+        case S_FINAL: mask = 1 | 8; break;
+    }
+    double v[4] = {0, 0, 0, 0};
+    for (int q = 0; q < 4; ++q)
+        if (mask >> q & 1) v[q] = a.faithful ? chunk_sum(a, q) : sum_slot(a, q, sh);
+    if (threadIdx.x != 0) return;
+    switch (which) {
+        case S_NORMB: st->norm_b = __dsqrt_rn(v[0]); break;
+        case S_NORMATB: st->norm_atb = __dsqrt_rn(v[0]); break;
+        case S_RHO: st->rho = v[2]; break;
+        case S_ALPHA: {
+            const double ww = v[0];
+            st->ww = ww;
+            if (ww == 0.0) { st->done = 1; st->zero_ww = 1; break; }
+            st->alpha = __ddiv_rn(st->rho, ww);
+            break;
+        }
+        case S_BETA: {
+            const double zz = v[1], zzt = v[2];
+            st->rr = v[3];
+            const long long it = st->it + 1;
+            const double normal_rel = __ddiv_rn(__dsqrt_rn(zz), st->norm_atb);
+            const double primal_rel = __ddiv_rn(__dsqrt_rn(v[3]), st->norm_b);
+            if (it - 1 < a.hist_len) { a.hist_n[it - 1] = normal_rel; a.hist_p[it - 1] = primal_rel; }
+            st->it = it;
+            st->zz = zz;
+            st->zzt = zzt;
+            if (normal_rel <= st->tol && (st->primal_tol < 0.0 || primal_rel <= st->primal_tol)) {
+                st->converged = 1;
+                st->done = 1;
+                break;
+            }
+            st->beta = st->rho != 0.0 ? __ddiv_rn(zzt, st->rho) : 0.0;
+            st->rho = zzt;
+            if (it >= st->max_iter) st->done = 1;
+            break;
+        }
+        case S_FINAL: st->zz = v[0]; st->rr = v[3]; break;
+    }
+}
+
+int launch_scalar(pn_context *c, int which, int faithful, int blas_threads, cudaStream_t s) {
+    ScalarArgs a;
+    a.partials = c->partials;
+    a.n_part = slot_stride(c);
+    a.chunks = c->ddot_chunks;
+    a.faithful = faithful;
+    a.nchunks = (c->R_l() <= 10000 || blas_threads <= 1) ? 1 : blas_threads;
+    a.hist_n = c->hist_n;
+    a.hist_p = c->hist_p;
+    a.hist_len = c->hist_len;
+    k_scalar<<<1, 256, 0, s>>>(which, a, c->state);
+    PN_CUDA(cudaGetLastError());
+    c->launches++;
+    return PN_OK;
+}
+
+// ------------------------------------------------------------ unstagger --
+// out [i][j][kl][c] (local slab, C-order); nested 0.5*(g + g_lower) in axis
+// order x, y, z with the lower sample replicated at global index 0.
+__global__ void k_unstagger(const int *__restrict__ par, Geo g, const double *__restrict__ u, double *__restrict__ out) {
+    const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long total = (long long)g.nx * g.ny * g.nzl * g.U;
+    if (q >= total) return;
+    const int c = (int)(q % g.U);
+    const long long vox = q / g.U;
+    const int kl = (int)(vox % g.nzl);
+    const int j = (int)((vox / g.nzl) % g.ny);
+    const int i = (int)(vox / ((long long)g.nzl * g.ny));
+    const int pc = par[c];
+    int ax[3], na = 0;
+    for (int a = 0; a < 3; ++a)
+        if (pc >> a & 1) ax[na++] = a;
+    const int n = 1 << na;
+    double gv[8];
+    for (int s = 0; s < n; ++s) {
+        int ii = i, jj = j, kk = g.z0 + kl;
+        for (int b = 0; b < na; ++b)
+            if (s >> b & 1) {
+                if (ax[b] == 0) ii = ii > 0 ? ii - 1 : 0;
+                if (ax[b] == 1) jj = jj > 0 ? jj - 1 : 0;
+                if (ax[b] == 2) kk = kk > 0 ? kk - 1 : 0;
+            }
+        gv[s] = u[((long long)(kk - g.z0) * g.pvox + (long long)jj * g.nx + ii) * g.U + c];
+    }
+    for (int b = 0; b < na; ++b)
+        for (int s = 0; s < n; ++s)
+            if (!(s >> b & 1)) gv[s] = __dmul_rn(0.5, __dadd_rn(gv[s], gv[s | (1 << b)]));
+    out[q] = gv[0];
+}
+
+int launch_unstagger(pn_context *c, const double *u, double *out, cudaStream_t s) {
+    long long total = (long long)c->g.nx * c->g.ny * c->g.nzl * c->U;
+    k_unstagger<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(c->tb.par, c->g, u, out);
+    PN_CUDA(cudaGetLastError());
+    c->launches++;
+    return PN_OK;
+}
+
+}  // namespace pn

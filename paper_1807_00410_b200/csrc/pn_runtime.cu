@@ -1,0 +1,636 @@
+// C ABI + solver driver of the B200 P_N path (include/pnrte_b200.h).
+//
+// The driver runs solve_normal_cg (pkg/src/pnrte/solver.py:189-257) entirely
+// on the device: every scalar (rho, alpha, beta, norms, the stop decision)
+// lives in a device State updated by one-block scalar kernels, every
+// iteration kernel is predicated on the device stop flag, and the host only
+// polls that flag every `check_every` iterations.  Two modes:
+//   fast      segmented sm_100a stencil kernels (pn_seg.cu) or the
+//             table kernel, FMA, deterministic fixed-order reductions;
+//   faithful  scipy csr_matvec order without FMA, numpy-rounded axpys and an
+//             emulation of the reference's OpenBLAS ddot: the trajectory is
+//             bit-identical to the reference (tests/test_gpu_parity.py).
+// Multi-GPU: z-slabs, one context per rank; halos of the stencil input are
+// exchanged with NCCL send/recv and per-(plane, block) reduction partials are
+// all-gathered so every rank sums the same numbers in the same order (the
+// result is independent of the rank count).  A loopback group runs several
+// slab contexts on one device with device copies in place of NCCL.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "pn_internal.cuh"
+#include "pn_seg.cuh"
+
+namespace pn {
+
+static thread_local std::string g_err;
+void set_error(const std::string &msg) { g_err = msg; }
+
+#define PN_NCCL(call)                                                                 \
+    do {                                                                              \
+        ncclResult_t r_ = (call);                                                     \
+        if (r_ != ncclSuccess) {                                                      \
+            ::pn::set_error(std::string(#call) + ": " + ncclGetErrorString(r_));      \
+            return PN_ERR_NCCL;                                                       \
+        }                                                                             \
+    } while (0)
+
+template <typename T>
+static int dalloc(pn_context *c, T **p, size_t n) {
+    void *q = nullptr;
+    cudaError_t e = cudaMalloc(&q, std::max<size_t>(n, 1) * sizeof(T));
+    if (e != cudaSuccess) {
+        set_error(std::string("cudaMalloc(") + std::to_string(n * sizeof(T)) + " B): " + cudaGetErrorString(e));
+        return PN_ERR_NOMEM;
+    }
+    c->dev_allocs.push_back(q);
+    *p = (T *)q;
+    return PN_OK;
+}
+
+template <typename T>
+static int dcopy(pn_context *c, T **dst, const T *src, size_t n) {
+    PN_TRY(dalloc(c, dst, n));
+    if (n) PN_CUDA(cudaMemcpy(*dst, src, n * sizeof(T), cudaMemcpyHostToDevice));
+    return PN_OK;
+}
+
+static int alloc_buf(pn_context *c, Buf &b) {
+    if (b.alloc) return PN_OK;
+    size_t n = (size_t)(c->g.nzl + 2) * c->g.plane;
+    PN_TRY(dalloc(c, &b.alloc, n));
+    PN_CUDA(cudaMemset(b.alloc, 0, n * sizeof(double)));
+    b.p = b.alloc + c->g.plane;
+    return PN_OK;
+}
+
+// ------------------------------------------------------------------ comm --
+// Exchange of z-halo planes and reduction partials between slab contexts.
+static int halo_exchange(std::vector<pn_context *> &cs, Buf pn_context::*vec, cudaStream_t s) {
+    pn_context *c0 = cs[0];
+    if (c0->world <= 1) return PN_OK;
+    const size_t pb = (size_t)c0->g.plane * sizeof(double);
+    if (c0->nccl) {
+        pn_context *c = c0;
+        ncclComm_t comm = (ncclComm_t)c->nccl;
+        Buf &v = c->*vec;
+        PN_NCCL(ncclGroupStart());
+        if (c->rank > 0) {
+            PN_NCCL(ncclSend(v.p, c->g.plane, ncclDouble, c->rank - 1, comm, s));
+            PN_NCCL(ncclRecv(v.p - c->g.plane, c->g.plane, ncclDouble, c->rank - 1, comm, s));
+        }
+        if (c->rank < c->world - 1) {
+            PN_NCCL(ncclSend(v.p + (size_t)(c->g.nzl - 1) * c->g.plane, c->g.plane, ncclDouble, c->rank + 1, comm, s));
+            PN_NCCL(ncclRecv(v.p + (size_t)c->g.nzl * c->g.plane, c->g.plane, ncclDouble, c->rank + 1, comm, s));
+        }
+        PN_NCCL(ncclGroupEnd());
+        return PN_OK;
+    }
+    // loopback: all slabs live on this device
+    for (size_t r = 0; r + 1 < cs.size(); ++r) {
+        Buf &lo = cs[r]->*vec, &hi = cs[r + 1]->*vec;
+        PN_CUDA(cudaMemcpyAsync(hi.p - cs[r + 1]->g.plane, lo.p + (size_t)(cs[r]->g.nzl - 1) * cs[r]->g.plane, pb,
+                                cudaMemcpyDeviceToDevice, s));
+        PN_CUDA(cudaMemcpyAsync(lo.p + (size_t)cs[r]->g.nzl * cs[r]->g.plane, hi.p, pb, cudaMemcpyDeviceToDevice, s));
+    }
+    return PN_OK;
+}
+
+// slots: bit mask of reduction slots whose partials every rank needs
+static int gather_partials(std::vector<pn_context *> &cs, int slots, cudaStream_t s) {
+    pn_context *c0 = cs[0];
+    if (c0->world <= 1) return PN_OK;
+    const long long stride = (long long)c0->g.nz * c0->red_bx;
+    const long long cnt = (long long)c0->g.nzl * c0->red_bx;
+    for (int q = 0; q < RED_SLOTS; ++q) {
+        if (!(slots >> q & 1)) continue;
+        if (c0->nccl) {
+            double *base = c0->partials + q * stride;
+            PN_NCCL(ncclAllGather(base + (long long)c0->g.z0 * c0->red_bx, base, cnt, ncclDouble,
+                                  (ncclComm_t)c0->nccl, s));
+        } else {
+            for (auto *src : cs)
+                for (auto *dst : cs) {
+                    if (src == dst) continue;
+                    long long off = q * stride + (long long)src->g.z0 * src->red_bx;
+                    PN_CUDA(cudaMemcpyAsync(dst->partials + off, src->partials + off, cnt * sizeof(double),
+                                            cudaMemcpyDeviceToDevice, s));
+                }
+        }
+    }
+    return PN_OK;
+}
+
+static void pick_red_bx(pn_context *c) {
+    long long target = 2LL * 148 * 8;
+    long long bx = (target + c->g.nz - 1) / c->g.nz;
+    long long maxb = (c->g.plane + 255) / 256;
+    c->red_bx = (int)std::max(1LL, std::min(bx, maxb));
+}
+
+}  // namespace pn
+
+using namespace pn;
+
+extern "C" {
+
+const char *pn_last_error(void) { return g_err.c_str(); }
+
+int pn_nccl_unique_id(void *out128) {
+    ncclUniqueId id;
+    PN_NCCL(ncclGetUniqueId(&id));
+    memcpy(out128, &id, sizeof(id));
+    return PN_OK;
+}
+
+int pn_create(const pn_desc *d, pn_context **out) {
+    if (!d || !out) { set_error("null argument"); return PN_ERR_INVALID; }
+    if (d->U != (d->N + 1) * (d->N + 1) || d->nx < 1 || d->ny < 1 || d->nz < 1 || d->nz_local < 1 || d->z0 < 0 ||
+        d->z0 + d->nz_local > d->nz) {
+        set_error("invalid grid / slab");
+        return PN_ERR_INVALID;
+    }
+    if (d->n_fields > MAX_FIELDS) { set_error("too many fields"); return PN_ERR_UNSUPPORTED; }
+    if (d->world > 1 && d->nz % d->world != 0) { set_error("nz must be divisible by world size"); return PN_ERR_INVALID; }
+    PN_CUDA(cudaSetDevice(d->device));
+    pn_context *c = new pn_context();
+    c->N = d->N;
+    c->U = d->U;
+    c->h = d->h;
+    c->device = d->device;
+    c->rank = d->rank;
+    c->world = d->world < 1 ? 1 : d->world;
+    c->canonical_diag = d->canonical_diag;
+    c->n_fields = d->n_fields;
+    Geo &g = c->g;
+    g.U = d->U; g.nx = d->nx; g.ny = d->ny; g.nz = d->nz; g.z0 = d->z0; g.nzl = d->nz_local;
+    g.pvox = (long long)d->nx * d->ny;
+    g.plane = g.pvox * d->U;
+    c->h_par.assign(d->par, d->par + d->U);
+    c->h_lam.assign(d->lam, d->lam + d->U);
+    c->h_lidx.assign(d->lidx, d->lidx + d->U);
+    c->h_aw.assign(d->a_w, d->a_w + d->n_a);
+    c->h_tw.assign(d->t_w, d->t_w + d->n_t);
+    int st = PN_OK;
+    Tables &t = c->tb;
+    auto ci = [&](const int **dst, const int32_t *src, size_t n) {
+        if (st == PN_OK) { int *p; st = dcopy(c, &p, (const int *)src, n); *dst = p; }
+    };
+    auto cd = [&](const double **dst, const double *src, size_t n) {
+        if (st == PN_OK) { double *p; st = dcopy(c, &p, src, n); *dst = p; }
+    };
+    const size_t U = d->U;
+    ci(&t.par, d->par, U);
+    ci(&t.a_ptr, d->a_ptr, U + 1); ci(&t.a_tgt, d->a_tgt, d->n_a); ci(&t.a_dir, d->a_dir, d->n_a);
+    ci(&t.a_diag, d->a_diag, d->n_a); cd(&t.a_w, d->a_w, d->n_a);
+    ci(&t.t_ptr, d->t_ptr, U + 1); ci(&t.t_src, d->t_src, d->n_t); ci(&t.t_dir, d->t_dir, d->n_t);
+    ci(&t.t_diag, d->t_diag, d->n_t); cd(&t.t_w, d->t_w, d->n_t);
+    ci(&t.d_ptr, d->d_ptr, U + 1); ci(&t.r_ptr, d->r_ptr, U + 1);
+    ci(&t.hascoef, d->term_hascoef, d->n_terms); ci(&t.nf, d->term_nf, d->n_terms);
+    ci(&t.tf, d->term_f, 2 * (size_t)d->n_terms); ci(&t.tsite, d->term_site, 2 * (size_t)d->n_terms);
+    cd(&t.tcoef, d->term_coef, d->n_terms);
+    t.n_a = d->n_a;
+    t.n_t = d->n_t;
+    if (st == PN_OK) { double *p; st = dalloc(c, &p, U); t.lamp = p; }
+    if (st != PN_OK) { pn_destroy(c); return st; }
+    c->f.n = d->n_fields;
+    pick_red_bx(c);
+    if (pn_seg_red_blocks(c) > 0) c->red_bx = pn_seg_red_blocks(c);
+    st = dalloc(c, &c->partials, (size_t)RED_SLOTS * g.nz * c->red_bx);
+    if (st == PN_OK) st = dalloc(c, &c->ddot_chunks, 4 * 64);
+    if (st == PN_OK) st = dalloc(c, &c->state, 1);
+    if (st == PN_OK) st = dalloc(c, &c->diag, (size_t)c->R_l());
+    if (st == PN_OK) st = alloc_buf(c, c->b);
+    if (st == PN_OK && cudaMallocHost(&c->h_state, sizeof(State)) != cudaSuccess) st = PN_ERR_NOMEM;
+    if (st == PN_OK) {
+        cudaMemset(c->partials, 0, sizeof(double) * RED_SLOTS * g.nz * c->red_bx);
+        cudaMemset(c->state, 0, sizeof(State));
+    }
+    if (st == PN_OK && c->world > 1 && d->nccl_id) {
+        ncclUniqueId id;
+        memcpy(&id, d->nccl_id, sizeof(id));
+        ncclComm_t comm;
+        ncclResult_t r = ncclCommInitRank(&comm, c->world, id, c->rank);
+        if (r != ncclSuccess) {
+            set_error(std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+            st = PN_ERR_NCCL;
+        } else {
+            c->nccl = comm;
+        }
+    }
+    if (st != PN_OK) { pn_destroy(c); return st; }
+    *out = c;
+    return PN_OK;
+}
+
+int pn_destroy(pn_context *c) {
+    if (!c) return PN_OK;
+    cudaSetDevice(c->device);
+    cudaDeviceSynchronize();
+    if (c->nccl) ncclCommDestroy((ncclComm_t)c->nccl);
+    for (void *p : c->dev_allocs) cudaFree(p);
+    for (double *p : c->field_alloc) cudaFree(p);
+    if (c->h_state) cudaFreeHost(c->h_state);
+    pn_seg_release(c);
+    delete c;
+    return PN_OK;
+}
+
+int pn_set_field(pn_context *c, int32_t slot, int32_t kind, double scalar, const double *data, void *stream) {
+    if (!c || slot < 0 || slot >= c->n_fields) { set_error("bad field slot"); return PN_ERR_INVALID; }
+    cudaStream_t s = (cudaStream_t)stream;
+    PN_CUDA(cudaSetDevice(c->device));
+    c->f.kind[slot] = kind;
+    c->f.scalar[slot] = scalar;
+    c->f.data[slot] = nullptr;
+    if (kind == 1 && slot < 2) {
+        // sigma_t / sigma_s are read as arrays by the fast kernels
+        double *dst;
+        size_t n = (size_t)(c->g.nzl + 1) * c->g.pvox;
+        cudaError_t e = cudaMalloc(&dst, n * sizeof(double));
+        if (e != cudaSuccess) { set_error(cudaGetErrorString(e)); return PN_ERR_NOMEM; }
+        c->field_alloc.push_back(dst);
+        PN_TRY(launch_fill(dst, (long long)n, scalar, s));
+        c->f.kind[slot] = 2;
+        c->f.data[slot] = dst;
+    } else if (kind == 2) {
+        if (!data) { set_error("array field without data"); return PN_ERR_INVALID; }
+        double *dst;
+        size_t n = (size_t)(c->g.nzl + 1) * c->g.pvox;
+        cudaError_t e = cudaMalloc(&dst, n * sizeof(double));
+        if (e != cudaSuccess) { set_error(cudaGetErrorString(e)); return PN_ERR_NOMEM; }
+        c->field_alloc.push_back(dst);
+        PN_TRY(launch_field_slab(c, slot, data, dst, s));
+        c->f.data[slot] = dst;
+    }
+    c->setup_done = false;
+    return PN_OK;
+}
+
+int pn_setup(pn_context *c, void *stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    PN_CUDA(cudaSetDevice(c->device));
+    // lambda_l * p_l per comp when every phase field is uniform (fast diagonal)
+    c->uniform_phase = 1;
+    std::vector<double> lamp(c->U, 0.0);
+    for (int comp = 0; comp < c->U; ++comp) {
+        int slot = 2 + c->h_lidx[comp];
+        int kd = c->f.kind[slot];
+        if (kd == 2) c->uniform_phase = 0;
+        double p = kd == 1 ? c->f.scalar[slot] : 0.0;
+        lamp[comp] = c->h_lam[comp] * p;
+    }
+    PN_CUDA(cudaMemcpyAsync((void *)c->tb.lamp, lamp.data(), c->U * sizeof(double), cudaMemcpyHostToDevice, s));
+    if (c->f.kind[0] != 2 && c->f.kind[0] != 1) { set_error("sigma_t missing"); return PN_ERR_INVALID; }
+    PN_TRY(launch_setup(c, true, s));
+    PN_TRY(pn_seg_prepare(c, s));
+    c->setup_done = true;
+    return PN_OK;
+}
+
+int pn_export_diag_rhs(pn_context *c, double *diag, double *rhs, void *stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!c->setup_done) { set_error("pn_setup not called"); return PN_ERR_INVALID; }
+    size_t n = (size_t)c->R_l() * sizeof(double);
+    if (diag) PN_CUDA(cudaMemcpyAsync(diag, c->diag, n, cudaMemcpyDeviceToDevice, s));
+    if (rhs) PN_CUDA(cudaMemcpyAsync(rhs, c->b.p, n, cudaMemcpyDeviceToDevice, s));
+    return PN_OK;
+}
+
+int64_t pn_kernel_launches(pn_context *c) { return c ? c->launches : 0; }
+
+}  // extern "C"
+
+namespace pn {
+
+static int ensure_vectors(pn_context *c, bool jacobi) {
+    for (Buf *b : {&c->x, &c->r, &c->p, &c->z, &c->w, &c->tmp}) PN_TRY(alloc_buf(c, *b));
+    if (jacobi) {
+        PN_TRY(alloc_buf(c, c->zt));
+        PN_TRY(alloc_buf(c, c->minv));
+    }
+    return PN_OK;
+}
+
+// one operator apply on padded internal vectors of a slab group
+// red: 0 none, 1 ww -> slot 0, 2 z/zt -> slots 1,2
+static int group_apply(std::vector<pn_context *> &cs, int trans, int faithful, Buf pn_context::*in,
+                       Buf pn_context::*out, int red, bool jacobi, bool gated, cudaStream_t s, bool seg = false) {
+    PN_TRY(halo_exchange(cs, in, s));
+    for (auto *c : cs) {
+        const double *x = (c->*in).p;
+        double *y = (c->*out).p;
+        if (faithful) {
+            PN_TRY(launch_apply_faithful(c, trans, 0, x, y, s, gated));
+        } else if (seg) {
+            PN_TRY(pn_seg_apply(c, trans, x, y, red, jacobi ? c->minv.p : nullptr, jacobi ? c->zt.p : nullptr, gated, s));
+        } else {
+            PN_TRY(launch_apply_table(c, trans, 0, 0, x, y, red, jacobi ? c->minv.p : nullptr,
+                                      jacobi ? c->zt.p : nullptr, s, gated));
+        }
+    }
+    if (red == 1) PN_TRY(gather_partials(cs, 1, s));
+    if (red == 2) PN_TRY(gather_partials(cs, 2 | 4, s));
+    return PN_OK;
+}
+
+static int group_dot(std::vector<pn_context *> &cs, Buf pn_context::*a, Buf pn_context::*b, int slot, int faithful,
+                     const pn_solve_opts *o, bool gated, cudaStream_t s) {
+    for (auto *c : cs) {
+        if (faithful)
+            PN_TRY(launch_ddot_emul(c, (c->*a).p, (c->*b).p, c->R_l(), slot, o->blas_threads, o->blas_kernel, s, gated));
+        else
+            PN_TRY(launch_dot(c, (c->*a).p, (c->*b).p, slot, s, gated));
+    }
+    if (!faithful) PN_TRY(gather_partials(cs, 1 << slot, s));
+    return PN_OK;
+}
+
+static int group_scalar(std::vector<pn_context *> &cs, int which, int faithful, const pn_solve_opts *o, cudaStream_t s) {
+    for (auto *c : cs) PN_TRY(launch_scalar(c, which, faithful, o->blas_threads, s));
+    return PN_OK;
+}
+
+static int group_vec(std::vector<pn_context *> &cs, int op, Buf pn_context::*y, Buf pn_context::*a,
+                     Buf pn_context::*b, bool gated, cudaStream_t s) {
+    for (auto *c : cs)
+        PN_TRY(launch_vec(c, op, (c->*y).p, a ? (c->*a).p : nullptr, b ? (c->*b).p : nullptr, s, gated));
+    return PN_OK;
+}
+
+// one CGNR iteration (solver.py:231-253), every kernel predicated on done
+static int iteration(std::vector<pn_context *> &cs, const pn_solve_opts *o, bool jacobi, bool seg, cudaStream_t s) {
+    const int F = o->mode == 1;
+    Buf pn_context::*ZT = jacobi ? &pn_context::zt : &pn_context::z;
+    // w = A p ; ww
+    PN_TRY(group_apply(cs, 0, F, &pn_context::p, &pn_context::w, F ? 0 : 1, false, true, s, seg));
+    if (F) PN_TRY(group_dot(cs, &pn_context::w, &pn_context::w, 0, F, o, true, s));
+    PN_TRY(group_scalar(cs, S_ALPHA, F, o, s));
+    // x += alpha p ; r -= alpha w  (fast: fused with ||r||^2)
+    if (F) {
+        PN_TRY(group_vec(cs, V_AXPY_ALPHA, &pn_context::x, &pn_context::p, nullptr, true, s));
+        PN_TRY(group_vec(cs, V_AXMY_ALPHA, &pn_context::r, &pn_context::w, nullptr, true, s));
+    } else {
+        for (auto *c : cs) PN_TRY(launch_xr(c, s));
+        PN_TRY(gather_partials(cs, 8, s));
+    }
+    // z = A^T r ; zt = z * minv ; rho' = z.zt ; ||z||, ||r||
+    PN_TRY(group_apply(cs, 1, F, &pn_context::r, &pn_context::z, F ? 0 : 2, jacobi, true, s, seg));
+    if (F) {
+        if (jacobi) PN_TRY(group_vec(cs, V_MUL, &pn_context::zt, &pn_context::z, &pn_context::minv, true, s));
+        PN_TRY(group_dot(cs, &pn_context::z, ZT, 2, F, o, true, s));
+        PN_TRY(group_dot(cs, &pn_context::z, &pn_context::z, 1, F, o, true, s));
+        PN_TRY(group_dot(cs, &pn_context::r, &pn_context::r, 3, F, o, true, s));
+    }
+    PN_TRY(group_scalar(cs, S_BETA, F, o, s));
+    // p = zt + beta p
+    if (F) PN_TRY(group_vec(cs, V_P_UPDATE, &pn_context::p, ZT, nullptr, true, s));
+    else for (auto *c : cs) PN_TRY(launch_pupd(c, (c->*ZT).p, s));
+    return PN_OK;
+}
+
+// reference-layout src -> solve-layout dst (copy, or segmented transpose)
+static int to_solve_layout(pn_context *c, bool seg, const double *src, double *dst, cudaStream_t s) {
+    if (seg) return pn_seg_convert(c, 0, src, dst, s);
+    PN_CUDA(cudaMemcpyAsync(dst, src, c->R_l() * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    return PN_OK;
+}
+static int from_solve_layout(pn_context *c, bool seg, const double *src, double *dst, cudaStream_t s) {
+    if (seg) return pn_seg_convert(c, 1, src, dst, s);
+    PN_CUDA(cudaMemcpyAsync(dst, src, c->R_l() * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    return PN_OK;
+}
+
+static int solve_group(std::vector<pn_context *> &cs, const pn_solve_opts *o, const double *const *bs,
+                       const double *const *x0s, double *const *xs, pn_report *rep, double *hn, double *hp,
+                       int64_t cap, cudaStream_t s) {
+    auto t0 = std::chrono::steady_clock::now();
+    pn_context *c0 = cs[0];
+    if (!(o->tol > 0)) { set_error("tolerance must be positive"); return PN_ERR_INVALID; }
+    if (o->max_iter < 0) { set_error("max_iter must be >= 0"); return PN_ERR_INVALID; }
+    const int F = o->mode == 1;
+    if (F && c0->world > 1) { set_error("faithful mode is single-slab only"); return PN_ERR_UNSUPPORTED; }
+    if (F && (o->blas_threads < 1 || o->blas_threads > 64)) { set_error("blas_threads out of range"); return PN_ERR_INVALID; }
+    const bool jacobi = o->jacobi != 0;
+    bool seg = !F;
+    for (auto *c : cs) seg = seg && pn_seg_ok(c);
+    for (auto *c : cs) {
+        PN_CUDA(cudaSetDevice(c->device));
+        if (!c->setup_done) { set_error("pn_setup not called"); return PN_ERR_INVALID; }
+        PN_TRY(ensure_vectors(c, jacobi));
+        PN_TRY(alloc_buf(c, c->bs));
+        long long hl = std::max<long long>(1, std::min<long long>(o->max_iter, 1LL << 24));
+        if (hl > c->hist_len) {
+            PN_TRY(dalloc(c, &c->hist_n, hl));
+            PN_TRY(dalloc(c, &c->hist_p, hl));
+            c->hist_len = hl;
+        }
+        State h{};
+        h.tol = o->tol;
+        h.primal_tol = o->primal_tol;
+        h.max_iter = o->max_iter;
+        PN_CUDA(cudaMemcpyAsync(c->state, &h, sizeof(State), cudaMemcpyHostToDevice, s));
+    }
+    // b (caller RHS or the assembled Q) in the solve layout
+    for (size_t i = 0; i < cs.size(); ++i)
+        PN_TRY(to_solve_layout(cs[i], seg, (bs && bs[i]) ? bs[i] : cs[i]->b.p, cs[i]->bs.p, s));
+    // norm_b, A^T b, norm_atb
+    PN_TRY(group_dot(cs, &pn_context::bs, &pn_context::bs, 0, F, o, false, s));
+    PN_TRY(group_scalar(cs, S_NORMB, F, o, s));
+    PN_TRY(group_apply(cs, 1, F, &pn_context::bs, &pn_context::tmp, 0, false, false, s, seg));
+    PN_TRY(group_dot(cs, &pn_context::tmp, &pn_context::tmp, 0, F, o, false, s));
+    PN_TRY(group_scalar(cs, S_NORMATB, F, o, s));
+    PN_CUDA(cudaMemcpyAsync(c0->h_state, c0->state, sizeof(State), cudaMemcpyDeviceToHost, s));
+    PN_CUDA(cudaStreamSynchronize(s));
+    *rep = pn_report{};
+    if (c0->h_state->norm_atb == 0.0 || c0->h_state->norm_b == 0.0) {
+        for (size_t i = 0; i < cs.size(); ++i)
+            PN_CUDA(cudaMemsetAsync(xs[i], 0, cs[i]->R_l() * sizeof(double), s));
+        PN_CUDA(cudaStreamSynchronize(s));
+        rep->converged = 1;
+        rep->wall_time = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        return PN_OK;
+    }
+    if (jacobi) {
+        // minv = 1 / colsum(A o A), 0 -> 1 (solver.py:218-223), exact order, then solve layout
+        PN_TRY(group_vec(cs, V_FILL_ONE, &pn_context::tmp, nullptr, nullptr, false, s));
+        PN_TRY(halo_exchange(cs, &pn_context::tmp, s));
+        for (auto *c : cs) PN_TRY(launch_apply_faithful(c, 1, 1, c->tmp.p, c->w.p, s, false));
+        PN_TRY(group_vec(cs, V_RECIP_DIAG, &pn_context::tmp, &pn_context::w, nullptr, false, s));
+        for (auto *c : cs) PN_TRY(to_solve_layout(c, seg, c->tmp.p, c->minv.p, s));
+    }
+    // x = x0 ; r = b - A x ; z = A^T r ; zt ; p = zt ; rho = z.zt
+    for (size_t i = 0; i < cs.size(); ++i) {
+        if (x0s && x0s[i]) PN_TRY(to_solve_layout(cs[i], seg, x0s[i], cs[i]->x.p, s));
+        else PN_CUDA(cudaMemsetAsync(cs[i]->x.p, 0, cs[i]->R_l() * sizeof(double), s));
+    }
+    PN_TRY(group_apply(cs, 0, F, &pn_context::x, &pn_context::tmp, 0, false, false, s, seg));
+    PN_TRY(group_vec(cs, V_SUB, &pn_context::r, &pn_context::bs, &pn_context::tmp, false, s));
+    PN_TRY(group_apply(cs, 1, F, &pn_context::r, &pn_context::z, 0, false, false, s, seg));
+    Buf pn_context::*ZT = jacobi ? &pn_context::zt : &pn_context::z;
+    if (jacobi) PN_TRY(group_vec(cs, V_MUL, &pn_context::zt, &pn_context::z, &pn_context::minv, false, s));
+    PN_TRY(group_vec(cs, V_COPY, &pn_context::p, ZT, nullptr, false, s));
+    PN_TRY(group_dot(cs, &pn_context::z, ZT, 2, F, o, false, s));
+    PN_TRY(group_scalar(cs, S_RHO, F, o, s));
+    // iterate in batches; the host polls the device stop flag between them
+    if (o->max_iter > 0) {
+        long long batch = o->check_every > 0 ? o->check_every : 4;
+        long long issued = 0;
+        while (true) {
+            long long n = std::min<long long>(batch, o->max_iter - issued);
+            for (long long k = 0; k < n; ++k) PN_TRY(iteration(cs, o, jacobi, seg, s));
+            issued += n;
+            PN_CUDA(cudaMemcpyAsync(c0->h_state, c0->state, sizeof(State), cudaMemcpyDeviceToHost, s));
+            PN_CUDA(cudaStreamSynchronize(s));
+            if (c0->h_state->done || issued >= o->max_iter) break;
+            if (o->check_every <= 0) batch = std::min<long long>(batch * 2, 64);
+        }
+    }
+    // true residuals (solver.py:254-255)
+    PN_TRY(group_apply(cs, 0, F, &pn_context::x, &pn_context::tmp, 0, false, false, s, seg));
+    PN_TRY(group_vec(cs, V_SUB, &pn_context::tmp, &pn_context::tmp, &pn_context::bs, false, s));
+    PN_TRY(group_apply(cs, 1, F, &pn_context::tmp, &pn_context::w, 0, false, false, s, seg));
+    PN_TRY(group_dot(cs, &pn_context::w, &pn_context::w, 0, F, o, false, s));
+    PN_TRY(group_dot(cs, &pn_context::tmp, &pn_context::tmp, 3, F, o, false, s));
+    PN_TRY(group_scalar(cs, S_FINAL, F, o, s));
+    for (size_t i = 0; i < cs.size(); ++i) PN_TRY(from_solve_layout(cs[i], seg, cs[i]->x.p, xs[i], s));
+    PN_CUDA(cudaMemcpyAsync(c0->h_state, c0->state, sizeof(State), cudaMemcpyDeviceToHost, s));
+    PN_CUDA(cudaStreamSynchronize(s));
+    const State &h = *c0->h_state;
+    rep->iterations = h.it;
+    rep->converged = h.converged;
+    rep->normal_residual = std::sqrt(h.zz) / h.norm_atb;
+    rep->primal_residual = std::sqrt(h.rr) / h.norm_b;
+    long long nh = std::min<long long>(h.it, cap);
+    if (hn && nh > 0) PN_CUDA(cudaMemcpy(hn, c0->hist_n, nh * sizeof(double), cudaMemcpyDeviceToHost));
+    if (hp && nh > 0) PN_CUDA(cudaMemcpy(hp, c0->hist_p, nh * sizeof(double), cudaMemcpyDeviceToHost));
+    rep->wall_time = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return PN_OK;
+}
+
+}  // namespace pn
+
+extern "C" {
+
+int pn_apply(pn_context *c, int32_t transpose, int32_t mode, const double *x, double *y, void *stream) {
+    const double *xs[1] = {x};
+    double *ys[1] = {y};
+    return pn_group_apply(&c, 1, transpose, mode, xs, ys, stream);
+}
+
+int pn_group_apply(pn_context **ctxs, int32_t n, int32_t transpose, int32_t mode, const double **x, double **y,
+                   void *stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    std::vector<pn_context *> cs(ctxs, ctxs + n);
+    bool seg = mode != 1;
+    for (auto *c : cs) {
+        if (!c->setup_done) { set_error("pn_setup not called"); return PN_ERR_INVALID; }
+        PN_CUDA(cudaSetDevice(c->device));
+        PN_TRY(alloc_buf(c, c->tmp));
+        PN_TRY(alloc_buf(c, c->w));
+        seg = seg && pn_seg_ok(c);
+    }
+    for (int i = 0; i < n; ++i) PN_TRY(to_solve_layout(cs[i], seg, x[i], cs[i]->tmp.p, s));
+    PN_TRY(group_apply(cs, transpose, mode == 1, &pn_context::tmp, &pn_context::w, 0, false, false, s, seg));
+    for (int i = 0; i < n; ++i) PN_TRY(from_solve_layout(cs[i], seg, cs[i]->w.p, y[i], s));
+    return PN_OK;
+}
+
+int pn_jacobi_diag(pn_context *c, double *out, void *stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!c->setup_done) { set_error("pn_setup not called"); return PN_ERR_INVALID; }
+    PN_TRY(alloc_buf(c, c->tmp));
+    std::vector<pn_context *> cs{c};
+    PN_TRY(group_vec(cs, V_FILL_ONE, &pn_context::tmp, nullptr, nullptr, false, s));
+    PN_TRY(halo_exchange(cs, &pn_context::tmp, s));
+    PN_TRY(launch_apply_faithful(c, 1, 1, c->tmp.p, out, s, false));
+    return PN_OK;
+}
+
+int pn_solve(pn_context *c, const pn_solve_opts *o, const double *b, const double *x0, double *x, pn_report *rep,
+             double *hn, double *hp, int64_t cap, void *stream) {
+    std::vector<pn_context *> cs{c};
+    const double *bs[1] = {b};
+    const double *x0s[1] = {x0};
+    double *xs[1] = {x};
+    return solve_group(cs, o, bs, x0s, xs, rep, hn, hp, cap, (cudaStream_t)stream);
+}
+
+int pn_group_solve(pn_context **ctxs, int32_t n, const pn_solve_opts *o, double **x, pn_report *rep, double *hn,
+                   double *hp, int64_t cap, void *stream) {
+    std::vector<pn_context *> cs(ctxs, ctxs + n);
+    return solve_group(cs, o, nullptr, nullptr, x, rep, hn, hp, cap, (cudaStream_t)stream);
+}
+
+int pn_unstagger(pn_context *c, const double *u, double *out, void *stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    PN_TRY(alloc_buf(c, c->tmp));
+    PN_CUDA(cudaMemcpyAsync(c->tmp.p, u, c->R_l() * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    std::vector<pn_context *> cs{c};
+    PN_TRY(halo_exchange(cs, &pn_context::tmp, s));
+    return launch_unstagger(c, c->tmp.p, out, s);
+}
+
+int pn_solve_host(pn_context *c, const pn_solve_opts *o, double *x_host, pn_report *rep, double *hn, double *hp,
+                  int64_t cap) {
+    PN_CUDA(cudaSetDevice(c->device));
+    double *xd;
+    PN_CUDA(cudaMalloc(&xd, c->R_l() * sizeof(double)));
+    int st = pn_solve(c, o, nullptr, nullptr, xd, rep, hn, hp, cap, nullptr);
+    if (st == PN_OK) {
+        cudaError_t e = cudaMemcpy(x_host, xd, c->R_l() * sizeof(double), cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) { set_error(cudaGetErrorString(e)); st = PN_ERR_CUDA; }
+    }
+    cudaFree(xd);
+    return st;
+}
+
+// what: 0 = alternating A / A^T applies on internal vectors, 1 = fused CG
+// iterations (stop test disabled); returns average ms per apply / iteration
+int pn_bench(pn_context *c, int32_t what, int32_t reps, double *ms_per, void *stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!c->setup_done) { set_error("pn_setup not called"); return PN_ERR_INVALID; }
+    PN_TRY(ensure_vectors(c, false));
+    std::vector<pn_context *> cs{c};
+    const bool seg = pn_seg_ok(c);
+    cudaEvent_t e0, e1;
+    PN_CUDA(cudaEventCreate(&e0));
+    PN_CUDA(cudaEventCreate(&e1));
+    pn_solve_opts o{};
+    o.tol = 1e-300;
+    o.max_iter = 1LL << 40;
+    o.mode = 0;
+    // deterministic non-trivial inputs: p = r = b (solve layout)
+    PN_TRY(alloc_buf(c, c->bs));
+    PN_TRY(to_solve_layout(c, seg, c->b.p, c->bs.p, s));
+    PN_TRY(group_vec(cs, V_COPY, &pn_context::p, &pn_context::bs, nullptr, false, s));
+    PN_TRY(group_vec(cs, V_COPY, &pn_context::r, &pn_context::bs, nullptr, false, s));
+    if (what == 1) {
+        State h{};
+        h.tol = 1e-300; h.primal_tol = -1; h.max_iter = 1LL << 40; h.rho = 1.0; h.norm_b = 1.0; h.norm_atb = 1.0;
+        PN_CUDA(cudaMemcpyAsync(c->state, &h, sizeof(State), cudaMemcpyHostToDevice, s));
+    }
+    PN_CUDA(cudaEventRecord(e0, s));
+    for (int k = 0; k < reps; ++k) {
+        if (what == 0) PN_TRY(group_apply(cs, k & 1, 0, &pn_context::p, &pn_context::w, 0, false, false, s, seg));
+        else PN_TRY(iteration(cs, &o, false, seg, s));
+    }
+    PN_CUDA(cudaEventRecord(e1, s));
+    PN_CUDA(cudaEventSynchronize(e1));
+    float ms = 0;
+    PN_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    *ms_per = reps > 0 ? ms / reps : 0.0;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return PN_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,123 @@
+// Host side of the segmented fast operator: eligibility, parameter blocks,
+// launch dispatch per order N, and the reference <-> segmented layout
+// conversion (a 32 x U transpose inside each 32-voxel row).
+#include <cuda_runtime.h>
+
+#include <cstring>
+
+#include "pn_seg.cuh"
+#include "pn_seg_types.cuh"
+
+namespace pn {
+
+struct SegCtx {
+    SegParams *pa = nullptr, *pt = nullptr;   // host parameter blocks (A, A^T)
+    SegGeo g{};
+    bool ok = false;
+};
+
+static bool seg_geometry_ok(const pn_context *c) {
+    return c->g.nx % 32 == 0 && c->N >= 1 && c->N <= 7 && c->canonical_diag && c->tb.n_a <= SEG_MAXW &&
+           c->tb.n_t <= SEG_MAXW && c->U <= 64;
+}
+
+int pn_seg_red_blocks(const pn_context *c) {
+    if (!seg_geometry_ok(c)) return 0;
+    return (c->g.nx / 32) * ((c->g.ny + SEG_ROWS - 1) / SEG_ROWS);
+}
+
+bool pn_seg_ok(const pn_context *c) { return c->seg && ((SegCtx *)c->seg)->ok; }
+
+int pn_seg_prepare(pn_context *c, cudaStream_t) {
+    SegCtx *sc = (SegCtx *)c->seg;
+    if (!sc) {
+        sc = new SegCtx();
+        c->seg = sc;
+    }
+    sc->ok = false;
+    if (!seg_geometry_ok(c) || !c->uniform_phase || c->red_bx != pn_seg_red_blocks(c)) return PN_OK;
+    if (c->f.kind[0] != 2 || c->f.kind[1] != 2) return PN_OK;   // sigma arrays (uniform ones are materialised)
+    if (!sc->pa) {
+        sc->pa = new SegParams();
+        sc->pt = new SegParams();
+    }
+    memset(sc->pa, 0, sizeof(SegParams));
+    memset(sc->pt, 0, sizeof(SegParams));
+    for (size_t e = 0; e < c->h_aw.size(); ++e) sc->pa->w[e] = c->h_aw[e];
+    for (size_t e = 0; e < c->h_tw.size(); ++e) sc->pt->w[e] = c->h_tw[e];
+    std::vector<double> lamp(c->U);
+    PN_CUDA(cudaMemcpy(lamp.data(), c->tb.lamp, c->U * sizeof(double), cudaMemcpyDeviceToHost));
+    for (int q = 0; q < c->U; ++q) sc->pa->lamp[q] = sc->pt->lamp[q] = lamp[q];
+    SegGeo &g = sc->g;
+    g.U = c->U; g.nx = c->g.nx; g.ny = c->g.ny; g.nz = c->g.nz; g.z0 = c->g.z0; g.nzl = c->g.nzl;
+    g.nseg = c->g.nx / 32;
+    g.nyb = (c->g.ny + SEG_ROWS - 1) / SEG_ROWS;
+    g.plane = c->g.plane;
+    g.pvox = c->g.pvox;
+    sc->ok = true;
+    return PN_OK;
+}
+
+int pn_seg_apply(pn_context *c, int trans, const double *x, double *y, int red, const double *minv, double *zt,
+                 bool gated, cudaStream_t s) {
+    SegCtx *sc = (SegCtx *)c->seg;
+    const SegParams &prm = trans ? *sc->pt : *sc->pa;
+    const long long stride = (long long)c->g.nz * c->red_bx;
+    const State *st = gated ? c->state : nullptr;
+    const double *sig_t = c->f.data[0], *sig_s = c->f.data[1];
+    int rc;
+    switch (c->N) {
+#define PN_N(n)                                                                                                 \
+    case n:                                                                                                     \
+        rc = seg_launch<n>(prm, sc->g, trans, red, minv != nullptr, x, y, minv, zt, sig_t, sig_s, c->partials, \
+                           stride, c->red_bx, st, s);                                                           \
+        break;
+        PN_N(1) PN_N(2) PN_N(3) PN_N(4) PN_N(5) PN_N(6) PN_N(7)
+#undef PN_N
+        default: set_error("segmented kernel: unsupported order"); return PN_ERR_UNSUPPORTED;
+    }
+    c->launches++;
+    return rc;
+}
+
+// dir 0: reference layout (voxel-major, comp-minor) -> segmented; 1: back.
+__global__ void k_seg_convert(int dir, int U, const double *__restrict__ src, double *__restrict__ dst) {
+    extern __shared__ double tile[];   // 32 x (U+1)
+    const long long base = (long long)blockIdx.x * 32 * U;
+    const int n = 32 * U;
+    for (int t = threadIdx.x; t < n; t += blockDim.x) {
+        double v = src[base + t];
+        int l, c;
+        if (dir == 0) { l = t / U; c = t - l * U; }
+        else { c = t >> 5; l = t & 31; }
+        tile[l * (U + 1) + c] = v;
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < n; t += blockDim.x) {
+        int l, c;
+        if (dir == 0) { c = t >> 5; l = t & 31; }
+        else { l = t / U; c = t - l * U; }
+        dst[base + t] = tile[l * (U + 1) + c];
+    }
+}
+
+int pn_seg_convert(pn_context *c, int dir, const double *src, double *dst, cudaStream_t s) {
+    if (src == dst) { set_error("pn_seg_convert: in-place"); return PN_ERR_INVALID; }
+    long long rows = (long long)c->g.nzl * c->g.ny * (c->g.nx / 32);
+    size_t sm = (size_t)32 * (c->U + 1) * sizeof(double);
+    k_seg_convert<<<(unsigned)rows, 256, sm, s>>>(dir, c->U, src, dst);
+    PN_CUDA(cudaGetLastError());
+    c->launches++;
+    return PN_OK;
+}
+
+void pn_seg_release(pn_context *c) {
+    SegCtx *sc = (SegCtx *)c->seg;
+    if (!sc) return;
+    delete sc->pa;
+    delete sc->pt;
+    delete sc;
+    c->seg = nullptr;
+}
+
+}  // namespace pn

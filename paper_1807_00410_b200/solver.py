@@ -1,0 +1,373 @@
+"""Drop-in B200 runtime for the reference's solve path.
+
+Mirrors pnrte's runtime entry points (pkg/src/pnrte/__init__.py:21-25):
+
+    assemble(program, spec)                                   solver.py:96
+    solve_normal_cg(system, tol=1e-8, max_iter=50000,
+                    primal_tol=None, jacobi=False, x0=None)   solver.py:189-190
+    unstagger(u, program, res)                                solver.py:275
+    SparseSystem, SolveReport                                 solver.py:34-50
+
+with the same argument meaning, result types and error behaviour (ValueError
+for tol <= 0 or a dim mismatch, non-convergence reported in the report, zero
+RHS returns x = 0 converged).  ``assemble`` does not build a CSR matrix: it
+creates a device context holding the stencil tables and the fields, and the
+system's ``A`` is a matrix-free operator (``A @ x``, ``A.T @ x`` run the sm_100a
+kernels; ``A.to_scipy()`` exports the exact CSR for parity checks).
+
+Extra keyword arguments (all optional): ``mode`` ("fast" | "faithful"),
+``device`` and, for faithful runs, ``blas_threads`` / ``blas_kernel`` (the
+OpenBLAS configuration to reproduce bit for bit; default: this process's).
+
+PyTorch only provides device memory and the current stream; all compute is
+in libpnrte_b200.so (include/pnrte_b200.h).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .problems import field_slot
+from .program import as_tables, canonical_diag, field_slots, pack_tables
+
+SQRT_4PI = math.sqrt(4.0 * math.pi)
+
+
+@dataclass(frozen=True)
+class SparseSystem:
+    A: object               # StencilOperator (matrix-free, device)
+    Q: np.ndarray
+    res: tuple
+    n_unknowns: int
+
+
+@dataclass
+class SolveReport:
+    iterations: int = 0
+    converged: bool = False
+    normal_residual: float = math.inf
+    primal_residual: float = math.inf
+    wall_time: float = 0.0
+    normal_history: list = field(default_factory=list)
+    primal_history: list = field(default_factory=list)
+
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        raise RuntimeError("pnrte_b200 needs a CUDA device (B200, sm_100a); no CPU fallback exists")
+    return torch
+
+
+def _stream(torch):
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def blas_config():
+    """(threads, kernel) of this process's OpenBLAS, which the reference's
+    numpy uses; kernel 0 = SkylakeX, 1 = Haswell."""
+    try:
+        from threadpoolctl import threadpool_info
+        for info in threadpool_info():
+            if info.get("internal_api") == "openblas":
+                arch = (info.get("architecture") or "").lower()
+                return int(info["num_threads"]), (1 if arch in ("haswell", "zen") else 0)
+    except Exception:
+        pass
+    return 8, 0
+
+
+class PnContext:
+    """One device context (one GPU / one z-slab) of a P_N operator."""
+
+    def __init__(self, tables, res, h, device=0, z0=0, nz_local=None, rank=0, world=1, nccl_id=None):
+        torch = _torch()
+        L = _lib.load()
+        self.tables = tables
+        self.res = tuple(int(r) for r in res)
+        self.h = float(h)
+        self.U = tables.U
+        self.N = tables.N
+        self.device = int(device)
+        self.z0 = int(z0)
+        self.nz_local = int(nz_local if nz_local is not None else self.res[2])
+        self.R_local = self.res[0] * self.res[1] * self.nz_local * self.U
+        self.pk = pack_tables(tables, self.h)
+        pk = self.pk
+        d = _lib.Desc()
+        d.N, d.U = tables.N, tables.U
+        d.nx, d.ny, d.nz = self.res
+        d.z0, d.nz_local = self.z0, self.nz_local
+        d.h = self.h
+        d.device = self.device
+        d.n_fields = pk["n_fields"]
+        keep = []
+
+        def ptr(name):
+            a = np.ascontiguousarray(pk[name])
+            keep.append(a)
+            return a.ctypes.data_as(ctypes.c_void_p)
+
+        for name in ("par", "lam", "lidx", "a_ptr", "a_tgt", "a_dir", "a_diag", "a_w", "t_ptr", "t_src",
+                     "t_dir", "t_diag", "t_w", "d_ptr", "r_ptr", "term_hascoef", "term_nf", "term_f",
+                     "term_site", "term_coef"):
+            setattr(d, name, ptr(name))
+        d.n_a, d.n_t, d.n_terms = len(pk["a_w"]), len(pk["t_w"]), len(pk["term_coef"])
+        d.canonical_diag = int(canonical_diag(tables))
+        idbuf = None
+        if nccl_id is not None:
+            idbuf = ctypes.create_string_buffer(bytes(nccl_id), 128)
+            d.nccl_id = ctypes.cast(idbuf, ctypes.c_void_p)
+        d.rank, d.world = int(rank), int(world)
+        handle = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            _lib.check(L.pn_create(ctypes.byref(d), ctypes.byref(handle)))
+        self.handle = handle
+        self._L = L
+        self._torch = torch
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            try:
+                self._L.pn_destroy(h)
+            except Exception:
+                pass
+            self.handle = None
+
+    @property
+    def dev(self):
+        return self._torch.device("cuda", self.device)
+
+    def set_fields(self, spec):
+        """Upload every field slot (reference [i,j,k] C-order arrays)."""
+        torch = self._torch
+        held = []
+        with torch.cuda.device(self.device):
+            s = _stream(torch)
+            for slot, name in enumerate(field_slots(self.N)):
+                kind, scal, arr = field_slot(spec, name)
+                ptr = None
+                if kind == 2:
+                    t = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float64)).to(self.dev, non_blocking=False)
+                    held.append(t)
+                    ptr = ctypes.c_void_p(t.data_ptr())
+                _lib.check(self._L.pn_set_field(self.handle, slot, kind, scal, ptr, s))
+            _lib.check(self._L.pn_setup(self.handle, s))
+            torch.cuda.current_stream().synchronize()
+        del held
+
+    def empty(self):
+        return self._torch.empty(self.R_local, dtype=self._torch.float64, device=self.dev)
+
+    def apply(self, x, transpose=False, mode="fast"):
+        torch = self._torch
+        xt = torch.as_tensor(x, dtype=torch.float64, device=self.dev).contiguous()
+        y = self.empty()
+        with torch.cuda.device(self.device):
+            _lib.check(self._L.pn_apply(self.handle, int(bool(transpose)), 1 if mode == "faithful" else 0,
+                                        ctypes.c_void_p(xt.data_ptr()), ctypes.c_void_p(y.data_ptr()),
+                                        _stream(torch)))
+        return y
+
+    def diag_rhs(self):
+        d, r = self.empty(), self.empty()
+        with self._torch.cuda.device(self.device):
+            _lib.check(self._L.pn_export_diag_rhs(self.handle, ctypes.c_void_p(d.data_ptr()),
+                                                  ctypes.c_void_p(r.data_ptr()), _stream(self._torch)))
+        return d, r
+
+    def jacobi_diag(self):
+        out = self.empty()
+        with self._torch.cuda.device(self.device):
+            _lib.check(self._L.pn_jacobi_diag(self.handle, ctypes.c_void_p(out.data_ptr()), _stream(self._torch)))
+        return out
+
+    def solve(self, tol=1e-8, max_iter=50000, primal_tol=None, jacobi=False, x0=None, b=None, mode="fast",
+              blas_threads=None, blas_kernel=None, check_every=0):
+        torch = self._torch
+        o = _lib.SolveOpts()
+        o.tol = float(tol)
+        o.max_iter = int(max_iter)
+        o.primal_tol = -1.0 if primal_tol is None else float(primal_tol)
+        o.jacobi = int(bool(jacobi))
+        o.mode = 1 if mode == "faithful" else 0
+        th, kn = blas_config()
+        o.blas_threads = int(blas_threads if blas_threads is not None else th)
+        o.blas_kernel = int(blas_kernel if blas_kernel is not None else kn)
+        o.check_every = int(check_every)
+        x = self.empty()
+        x0t = None if x0 is None else torch.as_tensor(np.asarray(x0, dtype=np.float64) if not torch.is_tensor(x0)
+                                                      else x0, dtype=torch.float64, device=self.dev).contiguous()
+        bt = None if b is None else torch.as_tensor(b, dtype=torch.float64, device=self.dev).contiguous()
+        cap = max(1, min(int(max_iter), 1 << 24))
+        hn = np.zeros(cap)
+        hp = np.zeros(cap)
+        rep = _lib.Report()
+        with torch.cuda.device(self.device):
+            _lib.check(self._L.pn_solve(
+                self.handle, ctypes.byref(o),
+                None if bt is None else ctypes.c_void_p(bt.data_ptr()),
+                None if x0t is None else ctypes.c_void_p(x0t.data_ptr()),
+                ctypes.c_void_p(x.data_ptr()), ctypes.byref(rep),
+                hn.ctypes.data_as(ctypes.c_void_p), hp.ctypes.data_as(ctypes.c_void_p), cap, _stream(torch)))
+        it = int(rep.iterations)
+        report = SolveReport(iterations=it, converged=bool(rep.converged),
+                             normal_residual=float(rep.normal_residual), primal_residual=float(rep.primal_residual),
+                             wall_time=float(rep.wall_time), normal_history=hn[:it].tolist(),
+                             primal_history=hp[:it].tolist())
+        if rep.converged and it == 0 and not math.isfinite(report.normal_residual):
+            report.normal_residual = report.primal_residual = 0.0
+        return x, report
+
+    def unstagger(self, u):
+        torch = self._torch
+        ut = torch.as_tensor(u, dtype=torch.float64, device=self.dev).contiguous()
+        out = torch.empty((self.res[0], self.res[1], self.nz_local, self.U), dtype=torch.float64, device=self.dev)
+        with torch.cuda.device(self.device):
+            _lib.check(self._L.pn_unstagger(self.handle, ctypes.c_void_p(ut.data_ptr()),
+                                            ctypes.c_void_p(out.data_ptr()), _stream(torch)))
+        return out
+
+    def bench(self, what, reps):
+        ms = ctypes.c_double()
+        with self._torch.cuda.device(self.device):
+            _lib.check(self._L.pn_bench(self.handle, int(what), int(reps), ctypes.byref(ms), _stream(self._torch)))
+        return ms.value
+
+    def kernel_launches(self):
+        return int(self._L.pn_kernel_launches(self.handle))
+
+
+class StencilOperator:
+    """Matrix-free A (or A^T) of an assembled system; ``@`` runs on the GPU."""
+
+    def __init__(self, ctx, transpose=False):
+        self.ctx = ctx
+        self.transpose = transpose
+        n = ctx.R_local
+        self.shape = (n, n)
+
+    @property
+    def T(self):
+        return StencilOperator(self.ctx, not self.transpose)
+
+    def matvec(self, x, mode="fast"):
+        y = self.ctx.apply(x, transpose=self.transpose, mode=mode)
+        return y if self.ctx._torch.is_tensor(x) else y.cpu().numpy()
+
+    def __matmul__(self, x):
+        return self.matvec(x)
+
+    def to_scipy(self):
+        """Exact CSR of A as the reference assembles it (debug / parity)."""
+        import scipy.sparse as sp
+        ctx = self.ctx
+        diag = ctx.diag_rhs()[0].cpu().numpy()
+        A = _csr_from_tables(ctx.pk, ctx.res, diag)
+        return A.T.tocsr() if self.transpose else A
+
+
+def _csr_from_tables(pk, res, diag):
+    """Host-side CSR from the packed tables + device diagonal (vectorised
+    numpy; used only for exports / parity, not by the solve)."""
+    import scipy.sparse as sp
+    nx, ny, nz = res
+    U = pk["U"]
+    par = pk["par"]
+    v = np.arange(nx * ny * nz)
+    i, j, k = v % nx, (v // nx) % ny, v // (nx * ny)
+    bb = (i == nx - 1).astype(np.int32) | ((j == ny - 1).astype(np.int32) << 1) | ((k == nz - 1).astype(np.int32) << 2)
+    D = {0: (0, 0, 0), 1: (-1, 0, 0), 2: (1, 0, 0), 3: (0, -1, 0), 4: (0, 1, 0), 5: (0, 0, -1), 6: (0, 0, 1)}
+    rows, cols, vals = [], [], []
+    for c in range(U):
+        pinned_c = (par[c] & bb) != 0
+        for e in range(pk["a_ptr"][c], pk["a_ptr"][c + 1]):
+            t = pk["a_tgt"][e]
+            if pk["a_diag"][e]:
+                rows.append(v * U + c); cols.append(v * U + c); vals.append(diag[v * U + c])
+                continue
+            dx, dy, dz = D[int(pk["a_dir"][e])]
+            ii, jj, kk = i + dx, j + dy, k + dz
+            ok = (ii >= 0) & (jj >= 0) & (kk >= 0) & (ii < nx) & (jj < ny) & (kk < nz) & ~pinned_c
+            nbb = (ii == nx - 1).astype(np.int32) | ((jj == ny - 1).astype(np.int32) << 1) | \
+                ((kk == nz - 1).astype(np.int32) << 2)
+            ok &= (par[t] & nbb) == 0
+            u = ii + nx * (jj + ny * kk)
+            rows.append((v * U + c)[ok]); cols.append((u * U + t)[ok]); vals.append(np.full(ok.sum(), pk["a_w"][e]))
+    R = nx * ny * nz * U
+    A = sp.coo_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))), shape=(R, R)).tocsr()
+    A.sort_indices()
+    return A
+
+
+def _check_dim(program, spec):
+    dim = getattr(program, "dim", 3)
+    if len(tuple(spec.res)) != dim:
+        raise ValueError(f"problem is {len(tuple(spec.res))}-D but program is {dim}-D")
+
+
+def assemble(program, spec, device=0):
+    """Upload the stencil tables and fields and evaluate diagonal + RHS on the
+    device (solver.py:96-186).  Returns a SparseSystem whose A is matrix-free."""
+    _check_dim(program, spec)
+    if getattr(spec, "bc", "dirichlet") != "dirichlet":
+        raise NotImplementedError("matrix-free path implements vacuum (Dirichlet) boundaries")
+    tables = as_tables(program)
+    ctx = PnContext(tables, spec.res, spec.h, device=device)
+    ctx.set_fields(spec)
+    Q = ctx.diag_rhs()[1].cpu().numpy()
+    return SparseSystem(A=StencilOperator(ctx), Q=Q, res=tuple(spec.res), n_unknowns=tables.U)
+
+
+def solve_normal_cg(system, tol=1e-8, max_iter=50000, primal_tol=None, jacobi=False, x0=None, mode="fast",
+                    blas_threads=None, blas_kernel=None):
+    """CGNR on A^T A u = A^T Q fully on the device (solver.py:189-257)."""
+    if tol <= 0:
+        raise ValueError("tolerance must be positive")
+    A = system.A
+    if not isinstance(A, StencilOperator):
+        raise NotImplementedError("generic CSR systems: use a stencil system from assemble()")
+    ctx = A.ctx
+    b = None
+    t0 = time.perf_counter()
+    x, rep = ctx.solve(tol=tol, max_iter=max_iter, primal_tol=primal_tol, jacobi=jacobi, x0=x0, b=system.Q
+                       if system.Q is not None else b, mode=mode, blas_threads=blas_threads, blas_kernel=blas_kernel)
+    out = x.cpu().numpy()
+    rep.wall_time = time.perf_counter() - t0
+    return out, rep
+
+
+def unstagger(u, program, res, device=0):
+    """Collocated (*res, U) coefficients (solver.py:275-296) on the device."""
+    tables = as_tables(program)
+    ctx = PnContext(tables, res, 1.0, device=device)
+    return ctx.unstagger(u).cpu().numpy()
+
+
+def fluence(collocated):
+    """sqrt(4 pi) * L00 (solver.py:299-301)."""
+    return SQRT_4PI * collocated[..., 0]
+
+
+def solve_pn(program_or_N, spec, tol=1e-8, max_iter=50000, primal_tol=None, jacobi=False, x0=None,
+             mode="fast", device=0, return_staggered=False, **kw):
+    """The north-star entry point: order + fields in, (N+1)^2 collocated SH
+    coefficients per voxel out (cli.py:136-155 without file I/O)."""
+    _check_dim(program_or_N if not isinstance(program_or_N, int) else None or type("p", (), {"dim": 3}), spec)
+    tables = as_tables(program_or_N)
+    ctx = PnContext(tables, spec.res, spec.h, device=device)
+    ctx.set_fields(spec)
+    if tol <= 0:
+        raise ValueError("tolerance must be positive")
+    x, rep = ctx.solve(tol=tol, max_iter=max_iter, primal_tol=primal_tol, jacobi=jacobi, x0=x0, mode=mode, **kw)
+    coll = ctx.unstagger(x).cpu().numpy()
+    if return_staggered:
+        return coll, rep, x.cpu().numpy()
+    return coll, rep
