@@ -1,0 +1,53 @@
+"""Seeded small problems shared by the golden generator and the tests.
+
+Deterministic on every machine (numpy default_rng); no dependency on the
+reference, so the GPU box can rebuild the same inputs.
+"""
+
+import numpy as np
+
+from paper_1807_00410_b200.problems import ProblemSpec, phase_fields
+from paper_1807_00410_b200.program import q_name
+
+# (name, N, res, seed): ragged grids, single voxel, thin slabs, 32-wide rows
+# (segmented kernel) and grids above the OpenBLAS 10000-element threading cut
+CASES = [
+    ("p1_567", 1, (5, 6, 7), 11),
+    ("p1_111", 1, (1, 1, 1), 12),
+    ("p1_213", 1, (2, 1, 3), 13),
+    ("p2_445", 2, (4, 4, 5), 14),
+    ("p3_456", 3, (4, 5, 6), 15),
+    ("p3_333", 3, (3, 3, 3), 16),
+    ("p4_344", 4, (3, 4, 4), 17),
+    ("p5_345", 5, (3, 4, 5), 18),
+    ("p6_334", 6, (3, 3, 4), 19),
+    ("p7_343", 7, (3, 4, 3), 20),
+    ("p1_3286", 1, (32, 8, 6), 21),
+    ("p3_3245", 3, (32, 4, 5), 22),
+    ("p5_3233", 5, (32, 3, 3), 23),
+    ("p7_3222", 7, (32, 2, 2), 24),
+]
+
+
+def rand_spec(N, res, seed, g=0.6, q_frac=0.5, uniform_sigma=False):
+    """Heterogeneous sigma_t in [0.5, 20), albedo in [0, 0.99), HG phase g,
+    random emission on about q_frac of the (l, m) coefficients."""
+    rng = np.random.default_rng(seed)
+    if uniform_sigma:
+        st = np.full(res, 4.0)
+        ss = np.full(res, 3.0)
+    else:
+        st = rng.uniform(0.5, 20.0, res)
+        ss = st * rng.uniform(0.0, 0.99, res)
+    f = {"sigma_t": st, "sigma_s": ss}
+    f.update(phase_fields(g, N))
+    for l in range(N + 1):
+        for m in range(-l, l + 1):
+            if rng.random() < q_frac:
+                f[q_name(l, m)] = rng.normal(size=res)
+    return ProblemSpec(dim=3, origin=(0.0, 0.0, 0.0), extent=tuple(r * 0.125 for r in res), res=tuple(res),
+                       fields=f)
+
+
+def probe_vector(R, seed=99):
+    return np.random.default_rng(seed).normal(size=R)

@@ -1,0 +1,186 @@
+"""Solver semantics of the reference tests (test_solver.py) on the device
+path, edge cases, the drop-in API, and the slab decomposition (loopback
+group of z-slab contexts on one GPU: P slabs == 1 slab, bit for bit)."""
+
+import ctypes
+
+import numpy as np
+import pytest
+
+from cases import rand_spec
+from paper_1807_00410_b200.configs import make_config, solve_spec
+from paper_1807_00410_b200.problems import ProblemSpec, phase_fields
+from paper_1807_00410_b200.program import build_tables, q_name
+
+pytestmark = pytest.mark.gpu
+
+
+def homogeneous_spec(res, sigma_t=1.0, sigma_s=0.0, q=0.0, extent=1.0):
+    """test_solver.py:21-31."""
+    shape = (res,) * 3
+    f = {"sigma_t": np.full(shape, sigma_t), "sigma_s": np.full(shape, sigma_s),
+         "p_0": np.full(shape, 1 / np.sqrt(4 * np.pi)), q_name(0, 0): np.full(shape, q)}
+    return ProblemSpec(dim=3, origin=(0.0,) * 3, extent=(extent,) * 3, res=shape, fields=f)
+
+
+def test_single_voxel_is_diagonal():
+    """test_solver.py:38-45: 1x1x1 Dirichlet keeps only collision entries."""
+    from paper_1807_00410_b200.solver import assemble
+    s = assemble(build_tables(1), homogeneous_spec(1, sigma_t=1.0))
+    A = s.A.to_scipy().toarray()
+    np.testing.assert_allclose(A, np.eye(4), atol=1e-14)
+
+
+def test_center_row_p1_has_seven_nonzeros():
+    """test_solver.py:48-55."""
+    from paper_1807_00410_b200.solver import assemble
+    s = assemble(build_tables(1), homogeneous_spec(3))
+    assert s.A.to_scipy().getrow(13 * 4).nnz == 7
+
+
+def test_adjoint_consistency():
+    """test_solver.py:82-92 on the fast device operator."""
+    from paper_1807_00410_b200.solver import assemble
+    s = assemble(build_tables(3), rand_spec(3, (32, 5, 4), 3))
+    rng = np.random.default_rng(0)
+    for _ in range(5):
+        u, v = rng.normal(size=s.A.shape[0]), rng.normal(size=s.A.shape[0])
+        lhs, rhs = float((s.A @ u) @ v), float(u @ (s.A.T @ v))
+        assert abs(lhs - rhs) <= 1e-12 * (1 + abs(lhs))
+
+
+def test_nonconvergence_reported_not_raised():
+    from paper_1807_00410_b200.solver import assemble, solve_normal_cg
+    s = assemble(build_tables(3), rand_spec(3, (32, 4, 4), 5))
+    for mode in ("fast", "faithful"):
+        _, rep = solve_normal_cg(s, tol=1e-14, max_iter=3, mode=mode)
+        assert not rep.converged and rep.iterations == 3 and len(rep.normal_history) == 3
+
+
+def test_tol_must_be_positive():
+    from paper_1807_00410_b200.solver import assemble, solve_normal_cg
+    s = assemble(build_tables(1), homogeneous_spec(2))
+    with pytest.raises(ValueError):
+        solve_normal_cg(s, tol=0.0)
+
+
+def test_zero_rhs_returns_zero_converged():
+    """solver.py:211-216."""
+    from paper_1807_00410_b200.solver import assemble, solve_normal_cg
+    s = assemble(build_tables(1), homogeneous_spec(4, q=0.0))
+    x, rep = solve_normal_cg(s, tol=1e-8)
+    assert rep.converged and rep.iterations == 0 and not np.any(x)
+    assert rep.normal_residual == 0.0 and rep.primal_residual == 0.0
+
+
+def test_max_iter_zero_and_warm_start():
+    from paper_1807_00410_b200.solver import assemble, solve_normal_cg
+    s = assemble(build_tables(3), rand_spec(3, (32, 4, 3), 8))
+    x, rep = solve_normal_cg(s, tol=1e-10, max_iter=2000)
+    x2, rep2 = solve_normal_cg(s, tol=1e-10, max_iter=0, x0=x)
+    assert rep2.iterations == 0 and np.array_equal(x2, x)
+    _, rep3 = solve_normal_cg(s, tol=1e-6, max_iter=2000, x0=x)
+    assert rep3.iterations <= 1
+
+
+def test_primal_tol_and_histories():
+    """test_solver.py:148-155."""
+    from paper_1807_00410_b200.solver import assemble, solve_normal_cg
+    s = assemble(build_tables(1), rand_spec(1, (32, 6, 5), 9))
+    _, rep = solve_normal_cg(s, tol=1e-10, max_iter=5000, primal_tol=1e-12)
+    assert rep.converged and rep.normal_history[-1] <= 1e-10 and rep.primal_history[-1] <= 1e-12
+    assert len(rep.primal_history) == len(rep.normal_history) == rep.iterations
+
+
+def test_jacobi_consistent():
+    """test_solver.py:136-145."""
+    from paper_1807_00410_b200.solver import assemble, solve_normal_cg
+    s = assemble(build_tables(3), rand_spec(3, (32, 5, 4), 10))
+    x0, r0 = solve_normal_cg(s, tol=1e-12, max_iter=5000)
+    x1, r1 = solve_normal_cg(s, tol=1e-12, max_iter=5000, jacobi=True)
+    assert r0.converged and r1.converged
+    np.testing.assert_allclose(x0, x1, atol=1e-6 * np.abs(x0).max())
+
+
+def test_dim_mismatch_raises():
+    from paper_1807_00410_b200.solver import assemble
+    f = {"sigma_t": np.ones((3, 3)), "sigma_s": np.zeros((3, 3))}
+    spec2 = ProblemSpec(dim=2, origin=(0, 0), extent=(1, 1), res=(3, 3), fields=f)
+    with pytest.raises(ValueError):
+        assemble(build_tables(1), spec2)
+
+
+def test_uniform_fields_segmented_path():
+    """Scalar (0-d) sigma fields are materialised for the segmented kernel."""
+    from paper_1807_00410_b200.solver import PnContext
+    from oracle.oracle import StencilOracle
+    spec = rand_spec(5, (32, 4, 4), 12, uniform_sigma=True)
+    spec = ProblemSpec(3, spec.origin, spec.extent, spec.res,
+                       dict(spec.fields, sigma_t=np.float64(4.0), sigma_s=np.float64(3.0)))
+    c = PnContext(build_tables(5), spec.res, spec.h)
+    c.set_fields(spec)
+    o = StencilOracle(build_tables(5), spec)
+    x = np.random.default_rng(1).normal(size=o.R)
+    y = c.apply(x, 0, "fast").cpu().numpy()
+    assert np.linalg.norm(y - o.apply(x)) <= 1e-13 * np.linalg.norm(o.apply(x))
+
+
+def test_solve_pn_end_to_end():
+    """Order + fields in, collocated (N+1)^2 coefficients out (cli.py:136-155)."""
+    from paper_1807_00410_b200.solver import solve_pn
+    from oracle.oracle import StencilOracle
+    cfg = make_config(3, n=32)
+    spec = solve_spec(cfg)
+    coll, rep, xs = solve_pn(cfg.N, spec, tol=1e-6, max_iter=20000, return_staggered=True)
+    assert rep.converged and coll.shape == (32, 32, 32, 36)
+    o = StencilOracle(build_tables(cfg.N), spec)
+    assert coll.tobytes() == o.unstagger(xs).tobytes()
+
+
+def _group(tables, spec, n_slabs):
+    from paper_1807_00410_b200.solver import PnContext
+    nz = spec.res[2]
+    out = []
+    for r in range(n_slabs):
+        c = PnContext(tables, spec.res, spec.h, z0=r * nz // n_slabs, nz_local=nz // n_slabs, rank=r, world=n_slabs)
+        c.set_fields(spec)
+        out.append(c)
+    return out
+
+
+@pytest.mark.parametrize("N,res,slabs", [(1, (32, 8, 8), 2), (3, (32, 6, 8), 4), (7, (32, 4, 4), 2),
+                                         (3, (7, 5, 6), 3)])
+def test_loopback_slabs_match_single_slab(N, res, slabs):
+    """z-slab decomposition (halo planes + all-gathered plane partials) gives
+    the single-GPU result bit for bit, for the operator and the full solve."""
+    import torch
+    from paper_1807_00410_b200 import _lib
+    from paper_1807_00410_b200.solver import PnContext
+    spec = rand_spec(N, res, 31)
+    t = build_tables(N)
+    one = PnContext(t, res, spec.h)
+    one.set_fields(spec)
+    grp = _group(t, spec, slabs)
+    L = _lib.load()
+    x = torch.tensor(np.random.default_rng(2).normal(size=one.R_local), dtype=torch.float64, device="cuda")
+    R_l = grp[0].R_local
+    for mode in (0, 1):
+        for tr in (0, 1):
+            want = one.apply(x, tr, "faithful" if mode else "fast")
+            ys = [torch.empty(R_l, dtype=torch.float64, device="cuda") for _ in grp]
+            xs = [x[r * R_l:(r + 1) * R_l].contiguous() for r in range(slabs)]
+            hs = (ctypes.c_void_p * slabs)(*[g.handle.value for g in grp])
+            xp = (ctypes.c_void_p * slabs)(*[v.data_ptr() for v in xs])
+            yp = (ctypes.c_void_p * slabs)(*[v.data_ptr() for v in ys])
+            _lib.check(L.pn_group_apply(hs, slabs, tr, mode, xp, yp, None))
+            got = torch.cat(ys)
+            assert torch.equal(got, want), (mode, tr)
+    xo, ro = one.solve(tol=1e-9, max_iter=300, mode="fast")
+    xs = [torch.empty(R_l, dtype=torch.float64, device="cuda") for _ in grp]
+    opts = _lib.SolveOpts(1e-9, 300, -1.0, 0, 0, 8, 0, 0)
+    rep = _lib.Report()
+    hs = (ctypes.c_void_p * slabs)(*[g.handle.value for g in grp])
+    xp = (ctypes.c_void_p * slabs)(*[v.data_ptr() for v in xs])
+    _lib.check(L.pn_group_solve(hs, slabs, ctypes.byref(opts), xp, ctypes.byref(rep), None, None, 0, None))
+    assert rep.iterations == ro.iterations
+    assert torch.equal(torch.cat(xs), xo)

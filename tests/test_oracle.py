@@ -1,0 +1,109 @@
+"""The C oracle (oracle/pn_oracle.c) pinned against the reference: committed
+fixtures everywhere, the live reference where it is mounted."""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from cases import CASES, probe_vector, rand_spec
+from oracle.oracle import StencilOracle, ddot
+from paper_1807_00410_b200.configs import make_config
+from paper_1807_00410_b200.program import build_tables
+
+FIX_BLAS = (8, 0)   # fixtures were generated with OpenBLAS SkylakeX, 8 threads
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+@pytest.fixture(scope="module")
+def oracles():
+    return {name: StencilOracle(build_tables(N), rand_spec(N, res, seed)) for name, N, res, seed in CASES}
+
+
+@pytest.mark.parametrize("case", [c[0] for c in CASES])
+def test_oracle_assembly_matches_golden(case, oracles, golden):
+    o, g = oracles[case], golden["cases"]
+    A = o.csr()
+    assert np.array_equal(A.indptr, g[f"{case}/indptr"])
+    assert np.array_equal(A.indices, g[f"{case}/indices"])
+    assert A.data.tobytes() == g[f"{case}/data"].tobytes()
+    assert o.rhs.tobytes() == g[f"{case}/Q"].tobytes()
+    assert o.jacobi_diag().tobytes() == g[f"{case}/jac"].tobytes()
+
+
+@pytest.mark.parametrize("case", [c[0] for c in CASES])
+def test_oracle_apply_matches_golden(case, oracles, golden):
+    o, g = oracles[case], golden["cases"]
+    x = probe_vector(o.R)
+    assert o.apply(x).tobytes() == g[f"{case}/Ax"].tobytes()
+    assert o.apply(x, transpose=True).tobytes() == g[f"{case}/Atx"].tobytes()
+
+
+@pytest.mark.parametrize("case", [c[0] for c in CASES])
+def test_oracle_cgnr_matches_golden(case, oracles, golden):
+    o, g, meta = oracles[case], golden["cases"], golden["cases_meta"]["cases"][case]
+    for jac in (0, 1):
+        x, rep = o.cgnr(tol=1e-9, max_iter=400, jacobi=bool(jac), blas_threads=FIX_BLAS[0], blas_kernel=FIX_BLAS[1])
+        k = f"{case}/cg{jac}"
+        assert rep["iterations"] == meta[f"cg{jac}"]["iterations"]
+        assert x.tobytes() == g[k + "/x"].tobytes()
+        assert np.array(rep["normal_history"]).tobytes() == g[k + "/nh"].tobytes()
+        assert np.array(rep["primal_history"]).tobytes() == g[k + "/ph"].tobytes()
+        assert rep["normal_residual"] == meta[f"cg{jac}"]["normal_residual"]
+    xs = g[f"{case}/cg0/x"]
+    assert o.unstagger(xs).tobytes() == g[f"{case}/unstagger"].tobytes()
+
+
+def test_oracle_config1_bit_identical_to_reference(golden):
+    cfg = make_config(1)
+    want = golden["configs"]["cfg1"]
+    o = StencilOracle(build_tables(cfg.N), cfg.spec)
+    assert sha(o.rhs) == want["Q_sha256"]
+    x, rep = o.cgnr(tol=cfg.tol, max_iter=cfg.max_iter, blas_threads=FIX_BLAS[0], blas_kernel=FIX_BLAS[1])
+    assert rep["iterations"] == want["iterations"] == 169
+    assert sha(x) == want["x_sha256"]
+    assert rep["normal_history"] == want["normal_history"]
+
+
+@pytest.mark.parametrize("kernel", [0, 1])
+@pytest.mark.parametrize("threads", [1, 3, 8])
+def test_ddot_emulation_properties(kernel, threads):
+    """Exact on integer-valued data (no rounding anywhere), symmetric in its
+    arguments, and chunk results combine in order."""
+    rng = np.random.default_rng(threads)
+    for n in (0, 1, 15, 16, 17, 31, 33, 10000, 10001, 123457):
+        x = rng.integers(-8, 8, n).astype(float)
+        y = rng.integers(-8, 8, n).astype(float)
+        assert ddot(x, y, threads, kernel) == float(np.sum(x * y))
+        z = rng.normal(size=n)
+        assert ddot(z, x, threads, kernel) == ddot(x, z, threads, kernel)
+
+
+@pytest.mark.reference
+def test_ddot_emulation_matches_numpy_blas(ref):
+    from oracle.oracle import blas_pin
+    th, kn = blas_pin()
+    rng = np.random.default_rng(7)
+    for n in list(range(1, 80)) + [9999, 10000, 10001, 65537, 1000003]:
+        x = rng.normal(size=n)
+        y = rng.normal(size=n) * np.exp(rng.normal(size=n))
+        assert ddot(x, y, th, kn) == float(x @ y)
+        assert np.sqrt(ddot(x, x, th, kn)) == float(np.linalg.norm(x))
+
+
+@pytest.mark.reference
+@pytest.mark.parametrize("case", ["p3_456", "p7_343", "p5_3233"])
+def test_oracle_matches_live_reference(case, ref):
+    from pnrte.equations import build_pn
+    from pnrte.solver import assemble, solve_normal_cg
+    from pnrte.stencil import compile_program
+    _, N, res, seed = [c for c in CASES if c[0] == case][0]
+    spec = rand_spec(N, res, seed)
+    s = assemble(compile_program(build_pn(N, 3)), spec)
+    o = StencilOracle(build_tables(N), spec)
+    x, rep = o.cgnr(tol=1e-10, max_iter=500, jacobi=True)
+    xr, rr = solve_normal_cg(s, tol=1e-10, max_iter=500, jacobi=True)
+    assert rep["iterations"] == rr.iterations and x.tobytes() == xr.tobytes()

@@ -1,0 +1,57 @@
+"""Input contract and config generators."""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from paper_1807_00410_b200.configs import make_config, solve_spec
+from paper_1807_00410_b200.problems import (ProblemSpec, SingularRiskError, field_slot, floor_sigma_t,
+                                            validate_for_solve, zonal_phase_coefficients)
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(np.asarray(a)).tobytes()).hexdigest()
+
+
+@pytest.mark.reference
+def test_phase_coefficients_bit_identical(ref):
+    from pnrte.sh import zonal_phase_coefficients as z
+    for g in (0.0, 0.3, 0.6, 0.8, 0.9):
+        assert zonal_phase_coefficients(g, 8) == z(g, 8)
+
+
+@pytest.mark.parametrize("idx", [1, 2])
+def test_config_fields_pinned(idx, golden):
+    cfg = make_config(idx)
+    want = golden["configs"][f"cfg{idx}"]["fields_sha256"]
+    assert {k: sha(v) for k, v in sorted(cfg.spec.fields.items())} == want
+
+
+@pytest.mark.parametrize("idx", [3, 4])
+def test_small_cloud_configs_pinned(idx, golden):
+    cfg = make_config(idx, n=32)
+    want = golden["configs"][f"cfg{idx}_n32_fields_sha256"]
+    assert {k: sha(v) for k, v in sorted(cfg.spec.fields.items())} == want
+    st = cfg.spec.fields["sigma_t"]
+    assert 0.0 < float(np.mean(st == 0.0)) < 0.9      # genuine vacuum
+    with pytest.raises(SingularRiskError):
+        validate_for_solve(cfg.spec)
+    validate_for_solve(solve_spec(cfg))
+
+
+def test_spec_validation_mirrors_reference():
+    f = {"sigma_t": np.ones((2, 2, 2)), "sigma_s": np.full((2, 2, 2), 2.0)}
+    with pytest.raises(ValueError):
+        ProblemSpec(3, (0, 0, 0), (1, 1, 1), (2, 2, 2), f)
+    f = {"sigma_t": np.ones((2, 2, 2)), "sigma_s": np.zeros((2, 2, 2))}
+    with pytest.raises(ValueError):
+        ProblemSpec(3, (0, 0, 0), (1, 2, 1), (2, 2, 2), f)
+    s = ProblemSpec(3, (0, 0, 0), (1, 1, 1), (2, 2, 2), f)
+    assert field_slot(s, "Q_0_0") == (0, 0.0, None)
+    with pytest.raises(KeyError):
+        field_slot(s, "bogus")
+    with pytest.raises(ValueError):
+        floor_sigma_t(s, 0.0)
+    fl = floor_sigma_t(s, 3.0)
+    assert np.all(fl.field_array("sigma_t") == 3.0) and fl.sigma_t_floor == 3.0
