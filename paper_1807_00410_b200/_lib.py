@@ -7,10 +7,12 @@ visible, every entry point raises; there is no CPU fallback.
 from __future__ import annotations
 
 import ctypes
+import os
 import pathlib
 
 HERE = pathlib.Path(__file__).resolve().parent
-LIB_PATH = HERE / "_lib" / "libpnrte_b200.so"
+
+LIB_PATH = pathlib.Path(os.environ.get("PNRTE_LIB", HERE / "_lib" / "libpnrte_b200.so"))
 
 P = ctypes.c_void_p
 I32 = ctypes.c_int32

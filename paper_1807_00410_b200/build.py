@@ -15,7 +15,8 @@ import sys
 
 HERE = pathlib.Path(__file__).resolve().parent
 CSRC = HERE / "csrc"
-OUT_DIR = HERE / "_lib"
+OUT_DIR = pathlib.Path(os.environ.get("PNRTE_BUILD_DIR", HERE / "_lib"))
+EXTRA = os.environ.get("PNRTE_NVCC_FLAGS", "").split()
 LIB = OUT_DIR / "libpnrte_b200.so"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -41,6 +42,7 @@ def sources():
 def _flags(src, inc):
     f = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-I", str(CSRC), "-I", str(inc), *ARCH]
+    f += EXTRA
     if src.name == "pn_kernels.cu":
         f.append("-fmad=false")
     return f
@@ -53,7 +55,7 @@ def build(verbose=False, force=False):
     OUT_DIR.mkdir(exist_ok=True)
     objs = []
     jobs = []
-    deps = list(CSRC.glob("*.cuh")) + list((CSRC / "generated").glob("*.cuh"))
+    deps = list(CSRC.glob("*.cuh")) + list((CSRC / "generated").glob("*.cuh")) + list((CSRC / "generated").glob("*.h"))
     newest_dep = max(p.stat().st_mtime for p in deps)
     for src in sources():
         obj = OUT_DIR / (src.stem + ".o")

@@ -3,8 +3,10 @@
 // conversion (a 32 x U transpose inside each 32-voxel row).
 #include <cuda_runtime.h>
 
+#include <cmath>
 #include <cstring>
 
+#include "generated/pn_seg_wmap.h"
 #include "pn_seg.cuh"
 #include "pn_seg_types.cuh"
 
@@ -17,13 +19,12 @@ struct SegCtx {
 };
 
 static bool seg_geometry_ok(const pn_context *c) {
-    return c->g.nx % 32 == 0 && c->N >= 1 && c->N <= 7 && c->canonical_diag && c->tb.n_a <= SEG_MAXW &&
-           c->tb.n_t <= SEG_MAXW && c->U <= 64;
+    return c->g.nx % 32 == 0 && c->N >= 1 && c->N <= 7 && c->canonical_diag && c->U <= 64;
 }
 
 int pn_seg_red_blocks(const pn_context *c) {
     if (!seg_geometry_ok(c)) return 0;
-    return (c->g.nx / 32) * ((c->g.ny + SEG_ROWS - 1) / SEG_ROWS);
+    return (c->g.nx / 32) * ((c->g.ny + seg_rows(c->N) - 1) / seg_rows(c->N));
 }
 
 bool pn_seg_ok(const pn_context *c) { return c->seg && ((SegCtx *)c->seg)->ok; }
@@ -43,15 +44,25 @@ int pn_seg_prepare(pn_context *c, cudaStream_t) {
     }
     memset(sc->pa, 0, sizeof(SegParams));
     memset(sc->pt, 0, sizeof(SegParams));
-    for (size_t e = 0; e < c->h_aw.size(); ++e) sc->pa->w[e] = c->h_aw[e];
-    for (size_t e = 0; e < c->h_tw.size(); ++e) sc->pt->w[e] = c->h_tw[e];
+    // distinct weight magnitudes: |w_e * h^-1| of a representative entry e
+    for (int trans = 0; trans < 2; ++trans) {
+        int nw = 0;
+        const int *rep = seg_wrep(c->N, trans, &nw);
+        const std::vector<double> &tw = trans ? c->h_tw : c->h_aw;
+        SegParams *pp = trans ? sc->pt : sc->pa;
+        if (!rep || nw > SEG_MAXW) return PN_OK;
+        for (int u = 0; u < nw; ++u) {
+            if (rep[u] >= (int)tw.size()) return PN_OK;
+            pp->w[u] = std::fabs(tw[rep[u]]);
+        }
+    }
     std::vector<double> lamp(c->U);
     PN_CUDA(cudaMemcpy(lamp.data(), c->tb.lamp, c->U * sizeof(double), cudaMemcpyDeviceToHost));
     for (int q = 0; q < c->U; ++q) sc->pa->lamp[q] = sc->pt->lamp[q] = lamp[q];
     SegGeo &g = sc->g;
     g.U = c->U; g.nx = c->g.nx; g.ny = c->g.ny; g.nz = c->g.nz; g.z0 = c->g.z0; g.nzl = c->g.nzl;
     g.nseg = c->g.nx / 32;
-    g.nyb = (c->g.ny + SEG_ROWS - 1) / SEG_ROWS;
+    g.nyb = (c->g.ny + seg_rows(c->N) - 1) / seg_rows(c->N);
     g.plane = c->g.plane;
     g.pvox = c->g.pvox;
     sc->ok = true;

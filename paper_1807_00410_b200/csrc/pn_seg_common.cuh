@@ -23,17 +23,16 @@ namespace pn {
 
 
 struct SegRow {
-    const double *X;                        // own row + lane
-    const double *Xym, *Xyp, *Xzm, *Xzp;    // neighbour rows + lane (null outside the domain)
-    const double *Xprev, *Xnext;            // previous / next segment row base (null outside)
-    const double *st[4], *ss[4];            // sigma rows (sy + 2 sz), + lane, edge-replicated
-    const double *stn[4], *ssn[4];          // x+1 sample for lane 31 (next segment or itself)
+    const double *xs;                       // own row staged in shared memory, + lane
+    const double *eprev, *enext;            // shared: x-edge values of the adjacent segments [U]
+    const double *sig;                      // shared: sigma_t / sigma_s rows [2][4][33]
+    const double *Xym, *Xyp, *Xzm, *Xzp;    // neighbour rows in global memory + lane (null outside)
     double *Y;                              // output row + lane
     const double *minv;                     // Jacobi inverse diag row + lane
     double *zt;                             // z * minv row + lane
     const double *diag;                     // stored diagonal row + lane (DIAG_ARRAY)
     int lane;
-    bool bx, by, bz, by_p, bz_p;
+    bool bx, bx_p, by, bz, by_p, bz_p;      // last-face flags: own voxel, x+1, y+1 row, z+1 row
 };
 
 struct RedAcc {
@@ -48,42 +47,45 @@ __device__ __forceinline__ bool pinned(const SegRow &r) {
 }
 
 template <int PS>
-__device__ __forceinline__ double ld_own(const SegRow &r, int s) {
-    const double v = __ldg(r.X + s * 32);
-    return pinned<PS>(r) ? 0.0 : v;
+__device__ __forceinline__ bool pinned_yz(const SegRow &r) {
+    return ((PS & 2) && r.by) || ((PS & 4) && r.bz);
 }
 
-template <int PS, int SIDE>
-__device__ __forceinline__ double nb_x(const SegRow &r, double v, int s) {
+// own-voxel value of comp s as an off-diagonal input (0 on its last face).
+// BND = false: interior row, no face can be hit, no masks are evaluated.
+template <int PS, bool BND>
+__device__ __forceinline__ double ld_own(const SegRow &r, int s) {
+    const double v = r.xs[s * 32];
+    return (BND && pinned<PS>(r)) ? 0.0 : v;
+}
+
+// x neighbour (lane -+ 1) from the staged row, segment edges from eprev/enext
+// (zero-filled outside the domain)
+template <int PS, int SIDE, bool BND>
+__device__ __forceinline__ double nb_x(const SegRow &r, int s) {
+    if (BND && pinned_yz<PS>(r)) return 0.0;
     if (SIDE < 0) {
-        double n = __shfl_up_sync(0xffffffffu, v, 1);
-        if (r.lane == 0) {
-            n = 0.0;
-            if (r.Xprev && !(((PS & 2) && r.by) || ((PS & 4) && r.bz))) n = __ldg(r.Xprev + s * 32 + 31);
-        }
-        return n;
+        return r.lane == 0 ? r.eprev[s] : r.xs[s * 32 - 1];
     } else {
-        double n = __shfl_down_sync(0xffffffffu, v, 1);
-        if (r.lane == 31) {
-            n = 0.0;
-            if (r.Xnext && !(((PS & 2) && r.by) || ((PS & 4) && r.bz))) n = __ldg(r.Xnext + s * 32);
-        }
-        return n;
+        const double n = r.lane == 31 ? r.enext[s] : r.xs[s * 32 + 1];
+        return (BND && (PS & 1) && r.bx_p) ? 0.0 : n;
     }
 }
 
-template <int PS, int SIDE>
+template <int PS, int SIDE, bool BND>
 __device__ __forceinline__ double nb_y(const SegRow &r, int s) {
     const double *p = SIDE < 0 ? r.Xym : r.Xyp;
+    if (!BND) return __ldg(p + s * 32);
     if (!p) return 0.0;
     const double v = __ldg(p + s * 32);
     const bool pin = ((PS & 1) && r.bx) || ((PS & 2) && SIDE > 0 && r.by_p) || ((PS & 4) && r.bz);
     return pin ? 0.0 : v;
 }
 
-template <int PS, int SIDE>
+template <int PS, int SIDE, bool BND>
 __device__ __forceinline__ double nb_z(const SegRow &r, int s) {
     const double *p = SIDE < 0 ? r.Xzm : r.Xzp;
+    if (!BND) return __ldg(p + s * 32);
     if (!p) return 0.0;
     const double v = __ldg(p + s * 32);
     const bool pin = ((PS & 1) && r.bx) || ((PS & 2) && r.by) || ((PS & 4) && SIDE > 0 && r.bz_p);
@@ -91,6 +93,7 @@ __device__ __forceinline__ double nb_z(const SegRow &r, int s) {
 }
 
 // average of sigma_t / sigma_s over the staggered site set of class P
+// (shared rows q = sy + 2 sz, 33 entries: 32 lanes + the x+1 sample of lane 31)
 template <int P>
 __device__ __forceinline__ void class_avg(const SegRow &r, double &at, double &as) {
     double t_ = 0.0, s_ = 0.0;
@@ -99,14 +102,11 @@ __device__ __forceinline__ void class_avg(const SegRow &r, double &at, double &a
 #pragma unroll
         for (int sy = 0; sy < ((P & 2) ? 2 : 1); ++sy) {
             const int q = sy + 2 * sz;
-            const double t = __ldg(r.st[q]), s = __ldg(r.ss[q]);
-            t_ += t;
-            s_ += s;
+            t_ += r.sig[q * 33];
+            s_ += r.sig[132 + q * 33];
             if (P & 1) {
-                double tn = __shfl_down_sync(0xffffffffu, t, 1), sn = __shfl_down_sync(0xffffffffu, s, 1);
-                if (r.lane == 31) { tn = __ldg(r.stn[q]); sn = __ldg(r.ssn[q]); }
-                t_ += tn;
-                s_ += sn;
+                t_ += r.sig[q * 33 + 1];
+                s_ += r.sig[132 + q * 33 + 1];
             }
         }
     constexpr int n = 1 << (((P >> 0) & 1) + ((P >> 1) & 1) + ((P >> 2) & 1));
@@ -131,7 +131,7 @@ __device__ __forceinline__ void store_out(const SegRow &r, RedAcc &ra, int c, do
 }
 
 #define W(e) prm.w[e]
-#define DIAG(at, as, c, off) (DIAG_ARRAY ? __ldg(r.diag + (c) * 32) : fma(-prm.lamp[c], (as), (at)))
+#define DIAG(at, as, c) (DIAG_ARRAY ? __ldg(r.diag + (c) * 32) : fma(-prm.lamp[c], (as), (at)))
 #define STORE(c, a) store_out<RED, JAC>(r, ra, (c), (a))
 
 }  // namespace pn
@@ -140,54 +140,91 @@ __device__ __forceinline__ void store_out(const SegRow &r, RedAcc &ra, int c, do
 
 namespace pn {
 
+template <int N> struct SegTune { static constexpr int rows = seg_rows(N), minb = seg_minb(N); };
+
+template <int N>
+__host__ __device__ constexpr size_t seg_smem_per_warp() {
+    return sizeof(double) * ((size_t)32 * (N + 1) * (N + 1) + 2 * (N + 1) * (N + 1) + 2 * 4 * 33);
+}
+
 template <int N, int TRANS, int RED, bool JAC>
-__global__ void __launch_bounds__(256) k_seg(const __grid_constant__ SegParams prm, SegGeo g,
-                                             const double *__restrict__ X, double *__restrict__ Y,
-                                             const double *__restrict__ minv, double *__restrict__ zt,
-                                             const double *__restrict__ st, const double *__restrict__ ss,
-                                             double *__restrict__ partials, long long slot_stride, int rb,
-                                             const State *state) {
+__global__ void __launch_bounds__(32 * SegTune<N>::rows, SegTune<N>::minb) k_seg(
+    const __grid_constant__ SegParams prm, SegGeo g, const double *__restrict__ X, double *__restrict__ Y,
+    const double *__restrict__ minv, double *__restrict__ zt, const double *__restrict__ st,
+    const double *__restrict__ ss, double *__restrict__ partials, long long slot_stride, int rb, const State *state) {
     if (state && seg_stopped(state)) return;
+    constexpr int U = (N + 1) * (N + 1);
+    extern __shared__ __align__(16) double smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int seg = blockIdx.x, j = blockIdx.y * SEG_ROWS + warp, kl = blockIdx.z, kg = g.z0 + kl;
-    const long long rowlen = (long long)g.U * 32;
+    const int seg = blockIdx.x, j = blockIdx.y * SegTune<N>::rows + warp, kl = blockIdx.z, kg = g.z0 + kl;
+    constexpr long long rowlen = (long long)U * 32;
+    double *xs = smem + warp * (seg_smem_per_warp<N>() / sizeof(double));
+    double *ep = xs + 32 * U, *en = ep + U, *sg = en + U;
     RedAcc ra;
     if (j < g.ny) {
-        SegRow r;
         const long long rowbase = (((long long)kl * g.ny + j) * g.nseg + seg) * rowlen;
-        r.lane = lane;
-        r.X = X + rowbase + lane;
-        r.Xym = j > 0 ? r.X - g.nseg * rowlen : nullptr;
-        r.Xyp = j < g.ny - 1 ? r.X + g.nseg * rowlen : nullptr;
-        r.Xzm = kg > 0 ? r.X - g.plane : nullptr;
-        r.Xzp = kg < g.nz - 1 ? r.X + g.plane : nullptr;
-        r.Xprev = seg > 0 ? X + rowbase - rowlen : nullptr;
-        r.Xnext = seg < g.nseg - 1 ? X + rowbase + rowlen : nullptr;
+        const double *Xrow = X + rowbase;
+        // stage the own row (32*U doubles) in shared memory: 16-byte cp.async, L2 only
+        {
+            const unsigned sbase = (unsigned)__cvta_generic_to_shared(xs);
+#pragma unroll 4
+            for (int q = lane; q < 16 * U; q += 32) {
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sbase + 16 * q),
+                             "l"(Xrow + 2 * q));
+            }
+            asm volatile("cp.async.commit_group;\n" ::);
+        }
+        // x-edge values of the adjacent segments and the sigma rows, meanwhile
+        const bool has_prev = seg > 0, has_next = seg < g.nseg - 1;
+        for (int c = lane; c < U; c += 32) {
+            ep[c] = has_prev ? __ldg(Xrow - rowlen + c * 32 + 31) : 0.0;
+            en[c] = has_next ? __ldg(Xrow + rowlen + c * 32) : 0.0;
+        }
         const int i = seg * 32 + lane;
-        const bool last_seg = seg == g.nseg - 1;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             const int jj = min(j + (q & 1), g.ny - 1);
             const int kk = kl + (q >> 1);   // plane nzl exists (edge-replicated at upload)
             const long long vb = ((long long)kk * g.ny + jj) * g.nx + seg * 32;
-            r.st[q] = st + vb + lane;
-            r.ss[q] = ss + vb + lane;
-            r.stn[q] = st + vb + (last_seg ? 31 : 32);
-            r.ssn[q] = ss + vb + (last_seg ? 31 : 32);
+            sg[q * 33 + lane] = __ldg(st + vb + lane);
+            sg[132 + q * 33 + lane] = __ldg(ss + vb + lane);
+            if (lane == 0) {
+                const int off = has_next ? 32 : 31;   // x+1 of lane 31, edge-replicated at nx-1
+                sg[q * 33 + 32] = __ldg(st + vb + off);
+                sg[132 + q * 33 + 32] = __ldg(ss + vb + off);
+            }
         }
+        asm volatile("cp.async.wait_all;\n" ::);
+        __syncwarp();
+        SegRow r;
+        r.lane = lane;
+        r.xs = xs + lane;
+        r.eprev = ep;
+        r.enext = en;
+        r.sig = sg + lane;
+        const double *Xl = Xrow + lane;
+        r.Xym = j > 0 ? Xl - g.nseg * rowlen : nullptr;
+        r.Xyp = j < g.ny - 1 ? Xl + g.nseg * rowlen : nullptr;
+        r.Xzm = kg > 0 ? Xl - g.plane : nullptr;
+        r.Xzp = kg < g.nz - 1 ? Xl + g.plane : nullptr;
         r.Y = Y + rowbase + lane;
         r.minv = minv ? minv + rowbase + lane : nullptr;
         r.zt = zt ? zt + rowbase + lane : nullptr;
         r.diag = nullptr;
         r.bx = i == g.nx - 1;
+        r.bx_p = i + 1 == g.nx - 1;
         r.by = j == g.ny - 1;
         r.bz = kg == g.nz - 1;
         r.by_p = j + 1 == g.ny - 1;
         r.bz_p = kg + 1 == g.nz - 1;
-        seg_row<N, TRANS, RED, JAC, false>(r, prm, ra);
+        // warp-uniform: rows away from the last faces and the y/z domain
+        // ends take the mask-free code path
+        const bool interior = seg != g.nseg - 1 && j >= 1 && j <= g.ny - 3 && kg >= 1 && kg <= g.nz - 3;
+        if (interior) seg_row<N, TRANS, RED, JAC, false, false>(r, prm, ra);
+        else seg_row<N, TRANS, RED, JAC, false, true>(r, prm, ra);
     }
     if (RED) {
-        __shared__ double red[3][SEG_ROWS];
+        __shared__ double red[3][SegTune<N>::rows];
         double v0 = ra.s0, v1 = ra.s1, v2 = ra.s2;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
@@ -200,7 +237,7 @@ __global__ void __launch_bounds__(256) k_seg(const __grid_constant__ SegParams p
         if (threadIdx.x == 0) {
             double a0 = 0.0, a1 = 0.0, a2 = 0.0;
 #pragma unroll
-            for (int w = 0; w < SEG_ROWS; ++w) { a0 += red[0][w]; a1 += red[1][w]; a2 += red[2][w]; }
+            for (int w = 0; w < SegTune<N>::rows; ++w) { a0 += red[0][w]; a1 += red[1][w]; a2 += red[2][w]; }
             const long long idx = (long long)kg * rb + (long long)seg * g.nyb + blockIdx.y;
             if (RED == 1) partials[idx] = a0;
             if (RED == 2) { partials[1 * slot_stride + idx] = a1; partials[2 * slot_stride + idx] = a2; }
@@ -212,9 +249,19 @@ template <int N>
 int seg_launch(const SegParams &prm, const SegGeo &g, int trans, int red, bool jac, const double *x, double *y,
                const double *minv, double *zt, const double *st, const double *ss, double *partials,
                long long slot_stride, int rb, const State *state, cudaStream_t s) {
-    dim3 grid(g.nseg, g.nyb, g.nzl), block(32 * SEG_ROWS);
-#define PN_SEG_GO(T, R, J) \
-    k_seg<N, T, R, J><<<grid, block, 0, s>>>(prm, g, x, y, minv, zt, st, ss, partials, slot_stride, rb, state)
+    constexpr int rows = SegTune<N>::rows;
+    dim3 grid(g.nseg, g.nyb, g.nzl), block(32 * rows);
+    const size_t smem = rows * seg_smem_per_warp<N>();
+    if (g.nyb != (g.ny + rows - 1) / rows) { set_error("segmented launch: row blocking mismatch"); return PN_ERR_INVALID; }
+#define PN_SEG_GO(T, R, J)                                                                                   \
+    do {                                                                                                     \
+        static bool cfg_done = false;                                                                        \
+        if (!cfg_done) {                                                                                     \
+            cudaFuncSetAttribute(k_seg<N, T, R, J>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+            cfg_done = true;                                                                                 \
+        }                                                                                                    \
+        k_seg<N, T, R, J><<<grid, block, smem, s>>>(prm, g, x, y, minv, zt, st, ss, partials, slot_stride, rb, state); \
+    } while (0)
     if (!trans) {
         if (red == 1) PN_SEG_GO(0, 1, false);
         else PN_SEG_GO(0, 0, false);

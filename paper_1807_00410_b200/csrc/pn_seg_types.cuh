@@ -3,11 +3,20 @@
 
 namespace pn {
 
-constexpr int SEG_MAXW = 1024;
-constexpr int SEG_ROWS = 8;   // warps (rows along y) per CTA
+constexpr int SEG_MAXW = 128;   // distinct |weight| values per table (80 for P7)
+// Launch shape per order N: warps (32-voxel rows along y) per CTA and the
+// CTAs per SM the register budget targets.  Shared memory holds one staged
+// row per warp (32*U doubles + edges + sigma rows).
+#ifdef PN_SEG_ROWS_OVERRIDE
+__host__ __device__ constexpr int seg_rows(int) { return PN_SEG_ROWS_OVERRIDE; }
+__host__ __device__ constexpr int seg_minb(int) { return PN_SEG_MINB_OVERRIDE; }
+#else
+__host__ __device__ constexpr int seg_rows(int N) { return N <= 2 ? 8 : (N <= 4 ? 4 : 2); }
+__host__ __device__ constexpr int seg_minb(int N) { return N <= 2 ? 4 : (N <= 4 ? 4 : (N <= 6 ? 6 : 5)); }
+#endif
 
 struct SegParams {
-    double w[SEG_MAXW];   // table weights (a_w or t_w), exact reference values
+    double w[SEG_MAXW];   // distinct |a_w| (or |t_w|) magnitudes, exact reference values
     double lamp[64];      // lambda_l * p_l per comp
 };
 
