@@ -106,10 +106,12 @@ struct pn_context {
     // Krylov vectors (padded with z-halo planes)
     pn::Buf x, r, p, z, zt, w, tmp, minv;
     bool vecs_ready = false;
+    bool bench_ready = false;
 
     // reductions
     int red_bx = 0;               // blocks per plane for reductions
-    double *partials = nullptr;   // [nz * red_bx * RED_SLOTS] global layout
+    double *partials = nullptr;   // [RED_SLOTS][nz][red_bx] block partials (global plane index)
+    double *plane_sums = nullptr; // [RED_SLOTS][nz] level-1 sums (all-gathered across ranks)
     double *ddot_chunks = nullptr;// faithful ddot chunk results [4][64]
     pn::State *state = nullptr;   // device
     pn::State *h_state = nullptr; // pinned host mirror
@@ -136,12 +138,13 @@ namespace pn {
 // kernels (pn_kernels.cu)
 int launch_fill(double *p, long long n, double v, cudaStream_t s);
 int launch_field_slab(pn_context *c, int slot, const double *src, double *dst, cudaStream_t s);
-int launch_setup(pn_context *c, bool want_diag, cudaStream_t s);
+int launch_setup(pn_context *c, bool want_diag, bool want_rhs, cudaStream_t s);
 int launch_apply_table(pn_context *c, int trans, int faithful, int squared, const double *x, double *y, int red,
                        const double *minv, double *zt, cudaStream_t s, bool gated);
 int launch_apply_faithful(pn_context *c, int trans, int squared, const double *x, double *y,
                           cudaStream_t s, bool gated = false);
 int launch_xr(pn_context *c, cudaStream_t s);
+int launch_plane_sums(pn_context *c, int mask, cudaStream_t s);
 int launch_pupd(pn_context *c, const double *zt, cudaStream_t s);
 int launch_dot(pn_context *c, const double *a, const double *b, int slot, cudaStream_t s, bool gated = false);
 int launch_ddot_emul(pn_context *c, const double *a, const double *b, long long n, int slot, int threads,

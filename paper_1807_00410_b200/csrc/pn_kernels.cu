@@ -104,16 +104,18 @@ __global__ void k_setup(Tables T, Fields F, Geo g, double *diag, double *rhs) {
     int kl = (int)(v / g.pvox);
     int bb = boundary_bits(g, i, j, g.z0 + kl);
     if (diag) diag[row] = eval_terms(T, F, g, T.d_ptr[c], T.d_ptr[c + 1], i, j, kl);
-    double r = 0.0;
-    if (T.r_ptr[c + 1] > T.r_ptr[c]) r = -eval_terms(T, F, g, T.r_ptr[c], T.r_ptr[c + 1], i, j, kl);
-    rhs[row] = (T.par[c] & bb) ? 0.0 : r;
+    if (rhs) {
+        double r = 0.0;
+        if (T.r_ptr[c + 1] > T.r_ptr[c]) r = -eval_terms(T, F, g, T.r_ptr[c], T.r_ptr[c + 1], i, j, kl);
+        rhs[row] = (T.par[c] & bb) ? 0.0 : r;
+    }
 }
 
-int launch_setup(pn_context *c, bool want_diag, cudaStream_t s) {
+int launch_setup(pn_context *c, bool want_diag, bool want_rhs, cudaStream_t s) {
     long long R = c->R_l();
     int bs = 256;
     long long nb = (R + bs - 1) / bs;
-    k_setup<<<(unsigned)nb, bs, 0, s>>>(c->tb, c->f, c->g, want_diag ? c->diag : nullptr, c->b.p);
+    k_setup<<<(unsigned)nb, bs, 0, s>>>(c->tb, c->f, c->g, want_diag ? c->diag : nullptr, want_rhs ? c->b.p : nullptr);
     PN_CUDA(cudaGetLastError());
     c->launches++;
     return PN_OK;
@@ -275,7 +277,8 @@ int launch_apply_table(pn_context *c, int trans, int faithful, int squared, cons
     dim3 grid(c->red_bx, c->g.nzl);
     size_t sm = table_smem(c, trans);
     const State *st = gated ? c->state : nullptr;
-    bool recompute = !faithful && c->canonical_diag && c->uniform_phase && c->diag == nullptr;
+    bool recompute = !faithful && c->canonical_diag && c->uniform_phase;
+    if (!recompute && !c->diag_ready) { set_error("internal: diagonal not assembled"); return PN_ERR_INVALID; }
     if (faithful) {
         k_apply_table<true, false><<<grid, 256, sm, s>>>(c->tb, c->f, c->g, trans, squared, x, y, c->diag, red, minv,
                                                          zt, c->partials, slot_stride(c), c->red_bx, st);
@@ -492,6 +495,37 @@ int launch_ddot_emul(pn_context *c, const double *a, const double *b, long long 
     return PN_OK;
 }
 
+// ---------------------------------------------------------- plane sums --
+// Level 1 of every fast reduction: the block partials of one z-plane are
+// summed in a fixed order into plane_sums[slot][kg].  The scalar kernels sum
+// the nz plane values (level 2); multi-GPU ranks all-gather plane sums, so
+// the result does not depend on the slab decomposition.
+__global__ void __launch_bounds__(256) k_plane_sums(const double *__restrict__ partials, double *__restrict__ plane_sums,
+                                                    long long slot_stride, int rb, int nz, int z0, int mask) {
+    const int slot = blockIdx.y;
+    if (!(mask >> slot & 1)) return;
+    const int kg = z0 + blockIdx.x;
+    const double *p = partials + slot * slot_stride + (long long)kg * rb;
+    __shared__ double sh[256];
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < rb; i += blockDim.x) acc = __dadd_rn(acc, p[i]);
+    sh[threadIdx.x] = acc;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if (threadIdx.x < o) sh[threadIdx.x] = __dadd_rn(sh[threadIdx.x], sh[threadIdx.x + o]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) plane_sums[slot * nz + kg] = sh[0];
+}
+
+int launch_plane_sums(pn_context *c, int mask, cudaStream_t s) {
+    dim3 grid(c->g.nzl, RED_SLOTS);
+    k_plane_sums<<<grid, 256, 0, s>>>(c->partials, c->plane_sums, slot_stride(c), c->red_bx, c->g.nz, c->g.z0, mask);
+    PN_CUDA(cudaGetLastError());
+    c->launches++;
+    return PN_OK;
+}
+
 // -------------------------------------------------------- scalar steps --
 // One block: fixed-order sums of the plane-block partials (fast) or the
 // in-order combination of ddot chunks (faithful), then the CGNR scalar logic
@@ -506,7 +540,7 @@ struct ScalarArgs {
 };
 
 __device__ double sum_slot(const ScalarArgs &a, int slot, double *sh) {
-    const double *p = a.partials + slot * a.n_part;
+    const double *p = a.partials + slot * a.n_part;   // plane sums of the slot
     double acc = 0.0;
     for (long long i = threadIdx.x; i < a.n_part; i += blockDim.x) acc = __dadd_rn(acc, p[i]);
     sh[threadIdx.x] = acc;
@@ -580,8 +614,8 @@ __global__ void __launch_bounds__(256) k_scalar(int which, ScalarArgs a, State *
 
 int launch_scalar(pn_context *c, int which, int faithful, int blas_threads, cudaStream_t s) {
     ScalarArgs a;
-    a.partials = c->partials;
-    a.n_part = slot_stride(c);
+    a.partials = c->plane_sums;
+    a.n_part = c->g.nz;
     a.chunks = c->ddot_chunks;
     a.faithful = faithful;
     a.nchunks = (c->R_l() <= 10000 || blas_threads <= 1) ? 1 : blas_threads;

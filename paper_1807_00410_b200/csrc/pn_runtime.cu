@@ -72,6 +72,13 @@ static int alloc_buf(pn_context *c, Buf &b) {
     return PN_OK;
 }
 
+static int ensure_diag(pn_context *c, cudaStream_t s) {
+    if (c->diag_ready) return PN_OK;
+    PN_TRY(launch_setup(c, true, false, s));
+    c->diag_ready = true;
+    return PN_OK;
+}
+
 // ------------------------------------------------------------------ comm --
 // Exchange of z-halo planes and reduction partials between slab contexts.
 static int halo_exchange(std::vector<pn_context *> &cs, Buf pn_context::*vec, cudaStream_t s) {
@@ -104,24 +111,24 @@ static int halo_exchange(std::vector<pn_context *> &cs, Buf pn_context::*vec, cu
     return PN_OK;
 }
 
-// slots: bit mask of reduction slots whose partials every rank needs
+// slots: bit mask of reduction slots every rank needs.  Block partials are
+// folded into per-plane sums locally; the plane sums are all-gathered.
 static int gather_partials(std::vector<pn_context *> &cs, int slots, cudaStream_t s) {
+    for (auto *c : cs) PN_TRY(launch_plane_sums(c, slots, s));
     pn_context *c0 = cs[0];
     if (c0->world <= 1) return PN_OK;
-    const long long stride = (long long)c0->g.nz * c0->red_bx;
-    const long long cnt = (long long)c0->g.nzl * c0->red_bx;
+    const long long nz = c0->g.nz, cnt = c0->g.nzl;
     for (int q = 0; q < RED_SLOTS; ++q) {
         if (!(slots >> q & 1)) continue;
         if (c0->nccl) {
-            double *base = c0->partials + q * stride;
-            PN_NCCL(ncclAllGather(base + (long long)c0->g.z0 * c0->red_bx, base, cnt, ncclDouble,
-                                  (ncclComm_t)c0->nccl, s));
+            double *base = c0->plane_sums + q * nz;
+            PN_NCCL(ncclAllGather(base + c0->g.z0, base, cnt, ncclDouble, (ncclComm_t)c0->nccl, s));
         } else {
             for (auto *src : cs)
                 for (auto *dst : cs) {
                     if (src == dst) continue;
-                    long long off = q * stride + (long long)src->g.z0 * src->red_bx;
-                    PN_CUDA(cudaMemcpyAsync(dst->partials + off, src->partials + off, cnt * sizeof(double),
+                    long long off = q * nz + src->g.z0;
+                    PN_CUDA(cudaMemcpyAsync(dst->plane_sums + off, src->plane_sums + off, cnt * sizeof(double),
                                             cudaMemcpyDeviceToDevice, s));
                 }
         }
@@ -205,6 +212,7 @@ int pn_create(const pn_desc *d, pn_context **out) {
     pick_red_bx(c);
     if (pn_seg_red_blocks(c) > 0) c->red_bx = pn_seg_red_blocks(c);
     st = dalloc(c, &c->partials, (size_t)RED_SLOTS * g.nz * c->red_bx);
+    if (st == PN_OK) st = dalloc(c, &c->plane_sums, (size_t)RED_SLOTS * g.nz);
     if (st == PN_OK) st = dalloc(c, &c->ddot_chunks, 4 * 64);
     if (st == PN_OK) st = dalloc(c, &c->state, 1);
     if (st == PN_OK) st = dalloc(c, &c->diag, (size_t)c->R_l());
@@ -212,6 +220,7 @@ int pn_create(const pn_desc *d, pn_context **out) {
     if (st == PN_OK && cudaMallocHost(&c->h_state, sizeof(State)) != cudaSuccess) st = PN_ERR_NOMEM;
     if (st == PN_OK) {
         cudaMemset(c->partials, 0, sizeof(double) * RED_SLOTS * g.nz * c->red_bx);
+        cudaMemset(c->plane_sums, 0, sizeof(double) * RED_SLOTS * g.nz);
         cudaMemset(c->state, 0, sizeof(State));
     }
     if (st == PN_OK && c->world > 1 && d->nccl_id) {
@@ -272,6 +281,7 @@ int pn_set_field(pn_context *c, int32_t slot, int32_t kind, double scalar, const
         c->f.data[slot] = dst;
     }
     c->setup_done = false;
+    c->diag_ready = false;
     return PN_OK;
 }
 
@@ -290,15 +300,21 @@ int pn_setup(pn_context *c, void *stream) {
     }
     PN_CUDA(cudaMemcpyAsync((void *)c->tb.lamp, lamp.data(), c->U * sizeof(double), cudaMemcpyHostToDevice, s));
     if (c->f.kind[0] != 2 && c->f.kind[0] != 1) { set_error("sigma_t missing"); return PN_ERR_INVALID; }
-    PN_TRY(launch_setup(c, true, s));
+    // the stored diagonal is only needed by the faithful path (and by the fast
+    // path when it cannot recompute the diagonal); it is assembled on demand
+    const bool need_diag = !(c->canonical_diag && c->uniform_phase);
+    PN_TRY(launch_setup(c, need_diag, true, s));
+    c->diag_ready = need_diag;
     PN_TRY(pn_seg_prepare(c, s));
     c->setup_done = true;
+    c->bench_ready = false;
     return PN_OK;
 }
 
 int pn_export_diag_rhs(pn_context *c, double *diag, double *rhs, void *stream) {
     cudaStream_t s = (cudaStream_t)stream;
     if (!c->setup_done) { set_error("pn_setup not called"); return PN_ERR_INVALID; }
+    if (diag) PN_TRY(ensure_diag(c, s));
     size_t n = (size_t)c->R_l() * sizeof(double);
     if (diag) PN_CUDA(cudaMemcpyAsync(diag, c->diag, n, cudaMemcpyDeviceToDevice, s));
     if (rhs) PN_CUDA(cudaMemcpyAsync(rhs, c->b.p, n, cudaMemcpyDeviceToDevice, s));
@@ -326,6 +342,7 @@ static int group_apply(std::vector<pn_context *> &cs, int trans, int faithful, B
                        Buf pn_context::*out, int red, bool jacobi, bool gated, cudaStream_t s, bool seg = false) {
     PN_TRY(halo_exchange(cs, in, s));
     for (auto *c : cs) {
+        if (faithful || !(c->canonical_diag && c->uniform_phase)) PN_TRY(ensure_diag(c, s));
         const double *x = (c->*in).p;
         double *y = (c->*out).p;
         if (faithful) {
@@ -463,7 +480,10 @@ static int solve_group(std::vector<pn_context *> &cs, const pn_solve_opts *o, co
         // minv = 1 / colsum(A o A), 0 -> 1 (solver.py:218-223), exact order, then solve layout
         PN_TRY(group_vec(cs, V_FILL_ONE, &pn_context::tmp, nullptr, nullptr, false, s));
         PN_TRY(halo_exchange(cs, &pn_context::tmp, s));
-        for (auto *c : cs) PN_TRY(launch_apply_faithful(c, 1, 1, c->tmp.p, c->w.p, s, false));
+        for (auto *c : cs) {
+            PN_TRY(ensure_diag(c, s));
+            PN_TRY(launch_apply_faithful(c, 1, 1, c->tmp.p, c->w.p, s, false));
+        }
         PN_TRY(group_vec(cs, V_RECIP_DIAG, &pn_context::tmp, &pn_context::w, nullptr, false, s));
         for (auto *c : cs) PN_TRY(to_solve_layout(c, seg, c->tmp.p, c->minv.p, s));
     }
@@ -549,6 +569,7 @@ int pn_jacobi_diag(pn_context *c, double *out, void *stream) {
     if (!c->setup_done) { set_error("pn_setup not called"); return PN_ERR_INVALID; }
     PN_TRY(alloc_buf(c, c->tmp));
     std::vector<pn_context *> cs{c};
+    PN_TRY(ensure_diag(c, s));
     PN_TRY(group_vec(cs, V_FILL_ONE, &pn_context::tmp, nullptr, nullptr, false, s));
     PN_TRY(halo_exchange(cs, &pn_context::tmp, s));
     PN_TRY(launch_apply_faithful(c, 1, 1, c->tmp.p, out, s, false));
@@ -608,12 +629,15 @@ int pn_bench(pn_context *c, int32_t what, int32_t reps, double *ms_per, void *st
     o.tol = 1e-300;
     o.max_iter = 1LL << 40;
     o.mode = 0;
-    // deterministic non-trivial inputs: p = r = b (solve layout)
-    PN_TRY(alloc_buf(c, c->bs));
-    PN_TRY(to_solve_layout(c, seg, c->b.p, c->bs.p, s));
-    PN_TRY(group_vec(cs, V_COPY, &pn_context::p, &pn_context::bs, nullptr, false, s));
-    PN_TRY(group_vec(cs, V_COPY, &pn_context::r, &pn_context::bs, nullptr, false, s));
-    if (what == 1) {
+    // deterministic non-trivial inputs: p = r = b (solve layout), once
+    if (!c->bench_ready) {
+        PN_TRY(alloc_buf(c, c->bs));
+        PN_TRY(to_solve_layout(c, seg, c->b.p, c->bs.p, s));
+        PN_TRY(group_vec(cs, V_COPY, &pn_context::p, &pn_context::bs, nullptr, false, s));
+        PN_TRY(group_vec(cs, V_COPY, &pn_context::r, &pn_context::bs, nullptr, false, s));
+        c->bench_ready = true;
+    }
+    if (what == 1 || what == 3) {
         State h{};
         h.tol = 1e-300; h.primal_tol = -1; h.max_iter = 1LL << 40; h.rho = 1.0; h.norm_b = 1.0; h.norm_atb = 1.0;
         PN_CUDA(cudaMemcpyAsync(c->state, &h, sizeof(State), cudaMemcpyHostToDevice, s));
@@ -621,6 +645,8 @@ int pn_bench(pn_context *c, int32_t what, int32_t reps, double *ms_per, void *st
     PN_CUDA(cudaEventRecord(e0, s));
     for (int k = 0; k < reps; ++k) {
         if (what == 0) PN_TRY(group_apply(cs, k & 1, 0, &pn_context::p, &pn_context::w, 0, false, false, s, seg));
+        else if (what == 2) PN_TRY(group_apply(cs, k & 1, 0, &pn_context::p, &pn_context::w, (k & 1) ? 2 : 1, false, false, s, seg));
+        else if (what == 3) PN_TRY(group_apply(cs, k & 1, 0, &pn_context::p, &pn_context::w, 0, false, true, s, seg));
         else PN_TRY(iteration(cs, &o, false, seg, s));
     }
     PN_CUDA(cudaEventRecord(e1, s));

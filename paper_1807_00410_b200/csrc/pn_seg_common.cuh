@@ -51,6 +51,14 @@ __device__ __forceinline__ bool pinned_yz(const SegRow &r) {
     return ((PS & 2) && r.by) || ((PS & 4) && r.bz);
 }
 
+__device__ __forceinline__ void cp_async16(void *dst_smem, const void *src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"((unsigned)__cvta_generic_to_shared(dst_smem)),
+                 "l"(src));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
 // own-voxel value of comp s as an off-diagonal input (0 on its last face).
 // BND = false: interior row, no face can be hit, no masks are evaluated.
 template <int PS, bool BND>
@@ -118,16 +126,19 @@ __device__ __forceinline__ void class_avg(const SegRow &r, double &at, double &a
 template <int RED, bool JAC>
 __device__ __forceinline__ void store_out(const SegRow &r, RedAcc &ra, int c, double a) {
     r.Y[c * 32] = a;
-    if (RED == 1) ra.s0 = fma(a, a, ra.s0);
-    if (RED == 2) {
-        double t = a;
-        if (JAC) {
-            t = a * __ldg(r.minv + c * 32);
-            r.zt[c * 32] = t;
-        }
+    if (RED == 2 && JAC) {   // Jacobi: zt = z * minv, z.zt and z.z per output
+        const double t = a * __ldg(r.minv + c * 32);
+        r.zt[c * 32] = t;
         ra.s2 = fma(a, t, ra.s2);
         ra.s1 = fma(a, a, ra.s1);
     }
+}
+
+// class-level reduction without Jacobi: RED 1 -> w.w, RED 2 -> z.z (= z.zt)
+template <int RED>
+__device__ __forceinline__ void seg_red_add(RedAcc &ra, double sq) {
+    if (RED == 1) ra.s0 += sq;
+    if (RED == 2) ra.s1 += sq;
 }
 
 #define W(e) prm.w[e]
@@ -152,7 +163,6 @@ __global__ void __launch_bounds__(32 * SegTune<N>::rows, SegTune<N>::minb) k_seg
     const __grid_constant__ SegParams prm, SegGeo g, const double *__restrict__ X, double *__restrict__ Y,
     const double *__restrict__ minv, double *__restrict__ zt, const double *__restrict__ st,
     const double *__restrict__ ss, double *__restrict__ partials, long long slot_stride, int rb, const State *state) {
-    if (state && seg_stopped(state)) return;
     constexpr int U = (N + 1) * (N + 1);
     extern __shared__ __align__(16) double smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -161,19 +171,20 @@ __global__ void __launch_bounds__(32 * SegTune<N>::rows, SegTune<N>::minb) k_seg
     double *xs = smem + warp * (seg_smem_per_warp<N>() / sizeof(double));
     double *ep = xs + 32 * U, *en = ep + U, *sg = en + U;
     RedAcc ra;
+    const long long rowbase = (((long long)kl * g.ny + j) * g.nseg + seg) * rowlen;
+    const double *Xrow = X + rowbase;
     if (j < g.ny) {
-        const long long rowbase = (((long long)kl * g.ny + j) * g.nseg + seg) * rowlen;
-        const double *Xrow = X + rowbase;
         // stage the own row (32*U doubles) in shared memory: 16-byte cp.async, L2 only
-        {
-            const unsigned sbase = (unsigned)__cvta_generic_to_shared(xs);
 #pragma unroll 4
-            for (int q = lane; q < 16 * U; q += 32) {
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sbase + 16 * q),
-                             "l"(Xrow + 2 * q));
-            }
-            asm volatile("cp.async.commit_group;\n" ::);
-        }
+        for (int q = lane; q < 16 * U; q += 32) cp_async16(xs + 2 * q, Xrow + 2 * q);
+        cp_async_commit();
+    }
+    // predicated on the solver's stop flag (CTA-uniform), read while the copy is in flight
+    if (state && seg_stopped(state)) {
+        cp_async_wait<0>();
+        return;
+    }
+    if (j < g.ny) {
         // x-edge values of the adjacent segments and the sigma rows, meanwhile
         const bool has_prev = seg > 0, has_next = seg < g.nseg - 1;
         for (int c = lane; c < U; c += 32) {
@@ -194,7 +205,7 @@ __global__ void __launch_bounds__(32 * SegTune<N>::rows, SegTune<N>::minb) k_seg
                 sg[132 + q * 33 + 32] = __ldg(ss + vb + off);
             }
         }
-        asm volatile("cp.async.wait_all;\n" ::);
+        cp_async_wait<0>();
         __syncwarp();
         SegRow r;
         r.lane = lane;
@@ -225,7 +236,7 @@ __global__ void __launch_bounds__(32 * SegTune<N>::rows, SegTune<N>::minb) k_seg
     }
     if (RED) {
         __shared__ double red[3][SegTune<N>::rows];
-        double v0 = ra.s0, v1 = ra.s1, v2 = ra.s2;
+        double v0 = ra.s0, v1 = ra.s1, v2 = (RED == 2 && !JAC) ? ra.s1 : ra.s2;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             v0 += __shfl_down_sync(0xffffffffu, v0, o);
