@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <algorithm>
 #include <cstring>
 
 #include "generated/pn_seg_wmap.h"
@@ -63,6 +64,10 @@ int pn_seg_prepare(pn_context *c, cudaStream_t) {
     g.U = c->U; g.nx = c->g.nx; g.ny = c->g.ny; g.nz = c->g.nz; g.z0 = c->g.z0; g.nzl = c->g.nzl;
     g.nseg = c->g.nx / 32;
     g.nyb = (c->g.ny + seg_rows(c->N) - 1) / seg_rows(c->N);
+    // planes above ~12 MB: march in z inside y-tiles of ~32 rows so the z
+    // neighbour rows stay in L2; smaller planes: plain (x, y, z) order
+    const double plane_mb = (double)c->g.plane * sizeof(double) / 1e6;
+    g.tyb = plane_mb > 12.0 ? std::min(g.nyb, std::max(1, 32 / seg_rows(c->N))) : g.nyb;
     g.plane = c->g.plane;
     g.pvox = c->g.pvox;
     sc->ok = true;

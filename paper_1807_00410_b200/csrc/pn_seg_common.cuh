@@ -151,7 +151,12 @@ __device__ __forceinline__ void seg_red_add(RedAcc &ra, double sq) {
 
 namespace pn {
 
-template <int N> struct SegTune { static constexpr int rows = seg_rows(N), minb = seg_minb(N); };
+template <int N> struct SegTune {
+    static constexpr int rows = seg_rows(N), minb = seg_minb(N);
+    static constexpr bool pair = seg_pair(N);
+    static constexpr int wpr = pair ? 2 : 1;         // warps per row
+    static constexpr int threads = 32 * rows * wpr;
+};
 
 template <int N>
 __host__ __device__ constexpr size_t seg_smem_per_warp() {
@@ -159,16 +164,29 @@ __host__ __device__ constexpr size_t seg_smem_per_warp() {
 }
 
 template <int N, int TRANS, int RED, bool JAC>
-__global__ void __launch_bounds__(32 * SegTune<N>::rows, SegTune<N>::minb) k_seg(
+__global__ void __launch_bounds__(SegTune<N>::threads, SegTune<N>::minb) k_seg(
     const __grid_constant__ SegParams prm, SegGeo g, const double *__restrict__ X, double *__restrict__ Y,
     const double *__restrict__ minv, double *__restrict__ zt, const double *__restrict__ st,
     const double *__restrict__ ss, double *__restrict__ partials, long long slot_stride, int rb, const State *state) {
     constexpr int U = (N + 1) * (N + 1);
     extern __shared__ __align__(16) double smem[];
+    constexpr int WPR = SegTune<N>::wpr;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int seg = blockIdx.x, j = blockIdx.y * SegTune<N>::rows + warp, kl = blockIdx.z, kg = g.z0 + kl;
+    const int rw = warp / WPR, half = warp % WPR;   // row within the CTA, class half
+    // L2-friendly traversal: CTAs march in z inside y-tiles of g.tyb row
+    // blocks, so the z-neighbour rows (k-1, k+1) are still in L2 when read
+    long long bid = blockIdx.x;
+    const int seg = (int)(bid % g.nseg);
+    bid /= g.nseg;
+    const int tyb = min(g.tyb, g.nyb);
+    const int jb_in = (int)(bid % tyb);
+    bid /= tyb;
+    const int kl = (int)(bid % g.nzl);
+    const int jb = (int)(bid / g.nzl) * tyb + jb_in;
+    const int j = jb < g.nyb ? jb * SegTune<N>::rows + rw : g.ny;
+    const int kg = g.z0 + kl;
     constexpr long long rowlen = (long long)U * 32;
-    double *xs = smem + warp * (seg_smem_per_warp<N>() / sizeof(double));
+    double *xs = smem + rw * (seg_smem_per_warp<N>() / sizeof(double));
     double *ep = xs + 32 * U, *en = ep + U, *sg = en + U;
     RedAcc ra;
     const long long rowbase = (((long long)kl * g.ny + j) * g.nseg + seg) * rowlen;
@@ -176,7 +194,7 @@ __global__ void __launch_bounds__(32 * SegTune<N>::rows, SegTune<N>::minb) k_seg
     if (j < g.ny) {
         // stage the own row (32*U doubles) in shared memory: 16-byte cp.async, L2 only
 #pragma unroll 4
-        for (int q = lane; q < 16 * U; q += 32) cp_async16(xs + 2 * q, Xrow + 2 * q);
+        for (int q = lane + 32 * half; q < 16 * U; q += 32 * WPR) cp_async16(xs + 2 * q, Xrow + 2 * q);
         cp_async_commit();
     }
     // predicated on the solver's stop flag (CTA-uniform), read while the copy is in flight
@@ -187,13 +205,16 @@ __global__ void __launch_bounds__(32 * SegTune<N>::rows, SegTune<N>::minb) k_seg
     if (j < g.ny) {
         // x-edge values of the adjacent segments and the sigma rows, meanwhile
         const bool has_prev = seg > 0, has_next = seg < g.nseg - 1;
-        for (int c = lane; c < U; c += 32) {
-            ep[c] = has_prev ? __ldg(Xrow - rowlen + c * 32 + 31) : 0.0;
-            en[c] = has_next ? __ldg(Xrow + rowlen + c * 32) : 0.0;
+        if (half == WPR - 1) {
+            for (int c = lane; c < U; c += 32) {
+                ep[c] = has_prev ? __ldg(Xrow - rowlen + c * 32 + 31) : 0.0;
+                en[c] = has_next ? __ldg(Xrow + rowlen + c * 32) : 0.0;
+            }
         }
         const int i = seg * 32 + lane;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
+            if (half != 0) break;
             const int jj = min(j + (q & 1), g.ny - 1);
             const int kk = kl + (q >> 1);   // plane nzl exists (edge-replicated at upload)
             const long long vb = ((long long)kk * g.ny + jj) * g.nx + seg * 32;
@@ -206,7 +227,8 @@ __global__ void __launch_bounds__(32 * SegTune<N>::rows, SegTune<N>::minb) k_seg
             }
         }
         cp_async_wait<0>();
-        __syncwarp();
+        if (WPR == 1) __syncwarp();
+        else asm volatile("bar.sync %0, %1;\n" ::"r"(1 + rw), "r"(32 * WPR) : "memory");
         SegRow r;
         r.lane = lane;
         r.xs = xs + lane;
@@ -231,11 +253,19 @@ __global__ void __launch_bounds__(32 * SegTune<N>::rows, SegTune<N>::minb) k_seg
         // warp-uniform: rows away from the last faces and the y/z domain
         // ends take the mask-free code path
         const bool interior = seg != g.nseg - 1 && j >= 1 && j <= g.ny - 3 && kg >= 1 && kg <= g.nz - 3;
-        if (interior) seg_row<N, TRANS, RED, JAC, false, false>(r, prm, ra);
-        else seg_row<N, TRANS, RED, JAC, false, true>(r, prm, ra);
+        if (WPR == 1) {
+            if (interior) seg_row<N, TRANS, RED, JAC, false, false>(r, prm, ra);
+            else seg_row<N, TRANS, RED, JAC, false, true>(r, prm, ra);
+        } else if (half == 0) {
+            if (interior) seg_half<N, TRANS, 0, RED, JAC, false, false>(r, prm, ra);
+            else seg_half<N, TRANS, 0, RED, JAC, false, true>(r, prm, ra);
+        } else {
+            if (interior) seg_half<N, TRANS, 1, RED, JAC, false, false>(r, prm, ra);
+            else seg_half<N, TRANS, 1, RED, JAC, false, true>(r, prm, ra);
+        }
     }
     if (RED) {
-        __shared__ double red[3][SegTune<N>::rows];
+        __shared__ double red[3][SegTune<N>::rows * SegTune<N>::wpr];
         double v0 = ra.s0, v1 = ra.s1, v2 = (RED == 2 && !JAC) ? ra.s1 : ra.s2;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
@@ -248,8 +278,8 @@ __global__ void __launch_bounds__(32 * SegTune<N>::rows, SegTune<N>::minb) k_seg
         if (threadIdx.x == 0) {
             double a0 = 0.0, a1 = 0.0, a2 = 0.0;
 #pragma unroll
-            for (int w = 0; w < SegTune<N>::rows; ++w) { a0 += red[0][w]; a1 += red[1][w]; a2 += red[2][w]; }
-            const long long idx = (long long)kg * rb + (long long)seg * g.nyb + blockIdx.y;
+            for (int w = 0; w < SegTune<N>::rows * SegTune<N>::wpr; ++w) { a0 += red[0][w]; a1 += red[1][w]; a2 += red[2][w]; }
+            const long long idx = (long long)kg * rb + (long long)seg * g.nyb + jb;
             if (RED == 1) partials[idx] = a0;
             if (RED == 2) { partials[1 * slot_stride + idx] = a1; partials[2 * slot_stride + idx] = a2; }
         }
@@ -261,7 +291,8 @@ int seg_launch(const SegParams &prm, const SegGeo &g, int trans, int red, bool j
                const double *minv, double *zt, const double *st, const double *ss, double *partials,
                long long slot_stride, int rb, const State *state, cudaStream_t s) {
     constexpr int rows = SegTune<N>::rows;
-    dim3 grid(g.nseg, g.nyb, g.nzl), block(32 * rows);
+    const long long ytiles = (g.nyb + g.tyb - 1) / g.tyb;
+    dim3 grid((unsigned)((long long)g.nseg * g.tyb * g.nzl * ytiles)), block(SegTune<N>::threads);
     const size_t smem = rows * seg_smem_per_warp<N>();
     if (g.nyb != (g.ny + rows - 1) / rows) { set_error("segmented launch: row blocking mismatch"); return PN_ERR_INVALID; }
 #define PN_SEG_GO(T, R, J)                                                                                   \

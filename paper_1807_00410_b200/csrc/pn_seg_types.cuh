@@ -10,9 +10,12 @@ constexpr int SEG_MAXW = 128;   // distinct |weight| values per table (80 for P7
 #ifdef PN_SEG_ROWS_OVERRIDE
 __host__ __device__ constexpr int seg_rows(int) { return PN_SEG_ROWS_OVERRIDE; }
 __host__ __device__ constexpr int seg_minb(int) { return PN_SEG_MINB_OVERRIDE; }
+__host__ __device__ constexpr bool seg_pair(int) { return PN_SEG_PAIR_OVERRIDE; }
 #else
-__host__ __device__ constexpr int seg_rows(int N) { return N <= 2 ? 8 : (N <= 4 ? 4 : 2); }
-__host__ __device__ constexpr int seg_minb(int N) { return N <= 2 ? 4 : (N <= 4 ? 4 : (N <= 6 ? 6 : 5)); }
+// pair: two warps share one staged row, each computing half of the classes
+__host__ __device__ constexpr bool seg_pair(int N) { return N >= 3; }
+__host__ __device__ constexpr int seg_rows(int N) { return N <= 2 ? 8 : 4; }
+__host__ __device__ constexpr int seg_minb(int N) { return N <= 2 ? 4 : (N <= 6 ? 3 : 2); }
 #endif
 
 struct SegParams {
@@ -22,6 +25,7 @@ struct SegParams {
 
 struct SegGeo {
     int U, nx, ny, nz, z0, nzl, nseg, nyb;
+    int tyb;                 // row blocks per y-tile of the CTA traversal
     long long plane, pvox;
 };
 
