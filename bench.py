@@ -165,7 +165,6 @@ def run_reference(args):
         return
     from paper_1807_00410_b200.configs import make_config
     cfg = make_config(4)
-    _, _, R, cores = cpu_oracle_rate(cfg, steps=1, warmup=0)
     rate, times, R, cores = cpu_oracle_rate(cfg, steps=args.steps, warmup=args.warmup)
     sample = f"cfg4 first {SAMPLE_PLANES} z-planes (256x256x{SAMPLE_PLANES}, P7, {R} unknowns), one apply per step"
     line = {

@@ -62,6 +62,7 @@ struct State {
     int done;               // stop flag: all iteration kernels become no-ops
     int converged;
     int zero_ww;
+    int xupd;               // fast path: x += alpha p still pending for this iteration
 };
 
 // number of fast-reduction partial slots per (plane, block)
@@ -124,6 +125,13 @@ struct pn_context {
 
     long long launches = 0;
 
+    // CUDA graph of a batch of CGNR iterations (single context, no NCCL)
+    cudaStream_t gstream = nullptr;
+    cudaEvent_t gev0 = nullptr, gev1 = nullptr;
+    cudaGraphExec_t gexec = nullptr;
+    long long gkey = -1;           // (mode, jacobi, seg, batch) the graph was captured for
+    long long graph_launches = 0;  // kernels per graph replay
+
     // segmented fast path (pn_seg.cu)
     void *seg = nullptr;
     pn::Buf bs;                   // RHS in the solve layout
@@ -144,6 +152,8 @@ int launch_apply_table(pn_context *c, int trans, int faithful, int squared, cons
 int launch_apply_faithful(pn_context *c, int trans, int squared, const double *x, double *y,
                           cudaStream_t s, bool gated = false);
 int launch_xr(pn_context *c, cudaStream_t s);
+int launch_r_update(pn_context *c, cudaStream_t s);
+int launch_xp_update(pn_context *c, const double *zt, cudaStream_t s);
 int launch_plane_sums(pn_context *c, int mask, cudaStream_t s);
 int launch_pupd(pn_context *c, const double *zt, cudaStream_t s);
 int launch_dot(pn_context *c, const double *a, const double *b, int slot, cudaStream_t s, bool gated = false);

@@ -349,6 +349,50 @@ __global__ void __launch_bounds__(256) k_xr(Geo g, double *__restrict__ x, doubl
     block_partials<1>(v, partials, sl, slot_stride, (long long)(g.z0 + kl) * rb + blockIdx.x);
 }
 
+// fast r -= alpha w with ||r||^2 partials (slot 3); x is updated later,
+// fused with the p update (k_xp), with the same alpha and p (bitwise equal)
+__global__ void __launch_bounds__(256) k_r(Geo g, double *__restrict__ r, const double *__restrict__ w,
+                                           const State *st, double *partials, long long slot_stride, int rb) {
+    if (stopped(st)) return;
+    const int kl = blockIdx.y;
+    const long long chunk = (g.plane + rb - 1) / rb;
+    const long long r0 = (long long)blockIdx.x * chunk;
+    const long long r1 = min(g.plane, r0 + chunk);
+    const long long base = (long long)kl * g.plane;
+    const double alpha = st->alpha;
+    double acc = 0.0;
+    for (long long rp = r0 + threadIdx.x; rp < r1; rp += blockDim.x) {
+        const long long i = base + rp;
+        const double rv = fma(-alpha, w[i], r[i]);
+        r[i] = rv;
+        acc = fma(rv, rv, acc);
+    }
+    double v[1] = {acc};
+    const int sl[1] = {3};
+    block_partials<1>(v, partials, sl, slot_stride, (long long)(g.z0 + kl) * rb + blockIdx.x);
+}
+
+// fast x += alpha p_old ; p = zt + beta p_old (p only while not stopped).
+// Runs after the stop test of the iteration, gated on st->xupd, which the
+// iteration's beta step sets and the next alpha step clears.
+__global__ void __launch_bounds__(256) k_xp(Geo g, double *__restrict__ x, double *__restrict__ p,
+                                            const double *__restrict__ zt, const State *st, int rb) {
+    if (*(volatile const int *)&st->xupd == 0) return;
+    const bool upd_p = !stopped(st);
+    const int kl = blockIdx.y;
+    const long long chunk = (g.plane + rb - 1) / rb;
+    const long long r0 = (long long)blockIdx.x * chunk;
+    const long long r1 = min(g.plane, r0 + chunk);
+    const long long base = (long long)kl * g.plane;
+    const double alpha = st->alpha, beta = st->beta;
+    for (long long rp = r0 + threadIdx.x; rp < r1; rp += blockDim.x) {
+        const long long i = base + rp;
+        const double pv = p[i];
+        x[i] = fma(alpha, pv, x[i]);
+        if (upd_p) p[i] = fma(beta, pv, zt[i]);
+    }
+}
+
 // fast p = zt + beta p
 __global__ void __launch_bounds__(256) k_pupd(Geo g, double *__restrict__ p, const double *__restrict__ zt,
                                               const State *st, int rb) {
@@ -394,6 +438,22 @@ int launch_xr(pn_context *c, cudaStream_t s) {
     dim3 grid(c->red_bx, c->g.nzl);
     k_xr<<<grid, 256, 0, s>>>(c->g, c->x.p, c->r.p, c->p.p, c->w.p, c->state, c->partials, slot_stride(c),
                               c->red_bx);
+    PN_CUDA(cudaGetLastError());
+    c->launches++;
+    return PN_OK;
+}
+
+int launch_r_update(pn_context *c, cudaStream_t s) {
+    dim3 grid(c->red_bx, c->g.nzl);
+    k_r<<<grid, 256, 0, s>>>(c->g, c->r.p, c->w.p, c->state, c->partials, slot_stride(c), c->red_bx);
+    PN_CUDA(cudaGetLastError());
+    c->launches++;
+    return PN_OK;
+}
+
+int launch_xp_update(pn_context *c, const double *zt, cudaStream_t s) {
+    dim3 grid(c->red_bx, c->g.nzl);
+    k_xp<<<grid, 256, 0, s>>>(c->g, c->x.p, c->p.p, zt, c->state, c->red_bx);
     PN_CUDA(cudaGetLastError());
     c->launches++;
     return PN_OK;
@@ -564,6 +624,7 @@ __device__ double chunk_sum(const ScalarArgs &a, int slot) {
 
 __global__ void __launch_bounds__(256) k_scalar(int which, ScalarArgs a, State *st) {
     __shared__ double sh[256];
+    if (which == S_ALPHA && threadIdx.x == 0) st->xupd = 0;   // previous iteration's x update has run
     if ((which == S_ALPHA || which == S_BETA) && stopped(st)) return;
     // slots each step consumes: 0 generic / ww, 1 zz, 2 zzt, 3 rr
     int mask = 0;
@@ -598,6 +659,7 @@ __global__ void __launch_bounds__(256) k_scalar(int which, ScalarArgs a, State *
             st->it = it;
             st->zz = zz;
             st->zzt = zzt;
+            st->xupd = 1;
             if (normal_rel <= st->tol && (st->primal_tol < 0.0 || primal_rel <= st->primal_tol)) {
                 st->converged = 1;
                 st->done = 1;

@@ -245,6 +245,10 @@ int pn_destroy(pn_context *c) {
     cudaSetDevice(c->device);
     cudaDeviceSynchronize();
     if (c->nccl) ncclCommDestroy((ncclComm_t)c->nccl);
+    if (c->gexec) cudaGraphExecDestroy(c->gexec);
+    if (c->gev0) cudaEventDestroy(c->gev0);
+    if (c->gev1) cudaEventDestroy(c->gev1);
+    if (c->gstream) cudaStreamDestroy(c->gstream);
     for (void *p : c->dev_allocs) cudaFree(p);
     for (double *p : c->field_alloc) cudaFree(p);
     if (c->h_state) cudaFreeHost(c->h_state);
@@ -396,7 +400,8 @@ static int iteration(std::vector<pn_context *> &cs, const pn_solve_opts *o, bool
         PN_TRY(group_vec(cs, V_AXPY_ALPHA, &pn_context::x, &pn_context::p, nullptr, true, s));
         PN_TRY(group_vec(cs, V_AXMY_ALPHA, &pn_context::r, &pn_context::w, nullptr, true, s));
     } else {
-        for (auto *c : cs) PN_TRY(launch_xr(c, s));
+        // r -= alpha w (+ ||r||^2); x += alpha p is fused into the p update below
+        for (auto *c : cs) PN_TRY(launch_r_update(c, s));
         PN_TRY(gather_partials(cs, 8, s));
     }
     // z = A^T r ; zt = z * minv ; rho' = z.zt ; ||z||, ||r||
@@ -408,9 +413,56 @@ static int iteration(std::vector<pn_context *> &cs, const pn_solve_opts *o, bool
         PN_TRY(group_dot(cs, &pn_context::r, &pn_context::r, 3, F, o, true, s));
     }
     PN_TRY(group_scalar(cs, S_BETA, F, o, s));
-    // p = zt + beta p
+    // p = zt + beta p   (fast: x += alpha p_old first, in the same pass)
     if (F) PN_TRY(group_vec(cs, V_P_UPDATE, &pn_context::p, ZT, nullptr, true, s));
-    else for (auto *c : cs) PN_TRY(launch_pupd(c, (c->*ZT).p, s));
+    else for (auto *c : cs) PN_TRY(launch_xp_update(c, (c->*ZT).p, s));
+    return PN_OK;
+}
+
+// Capture `gb` iterations once per (mode, jacobi, layout) on a private stream
+// and replay the graph until the device stop flag is set.
+static int run_graph_batches(pn_context *c, const pn_solve_opts *o, bool jacobi, bool seg, cudaStream_t s) {
+    std::vector<pn_context *> cs{c};
+    const long long per_it = 8;   // rough launches per iteration, to size batches
+    const long long gb = o->check_every > 0 ? o->check_every : (c->R_l() < (1LL << 22) ? 16 : 4);
+    (void)per_it;
+    const long long key = ((long long)o->mode << 40) | ((long long)jacobi << 39) | ((long long)seg << 38) |
+                          ((long long)o->blas_threads << 20) | ((long long)o->blas_kernel << 16) | gb;
+    if (!c->gstream) {
+        PN_CUDA(cudaStreamCreateWithFlags(&c->gstream, cudaStreamNonBlocking));
+        PN_CUDA(cudaEventCreateWithFlags(&c->gev0, cudaEventDisableTiming));
+        PN_CUDA(cudaEventCreateWithFlags(&c->gev1, cudaEventDisableTiming));
+    }
+    cudaStream_t g = c->gstream;
+    PN_CUDA(cudaEventRecord(c->gev0, s));
+    PN_CUDA(cudaStreamWaitEvent(g, c->gev0, 0));
+    if (c->gkey != key || !c->gexec) {
+        if (c->gexec) { cudaGraphExecDestroy(c->gexec); c->gexec = nullptr; }
+        cudaGraph_t graph;
+        const long long l0 = c->launches;
+        PN_CUDA(cudaStreamBeginCapture(g, cudaStreamCaptureModeThreadLocal));
+        int st = PN_OK;
+        for (long long k = 0; k < gb && st == PN_OK; ++k) st = iteration(cs, o, jacobi, seg, g);
+        cudaError_t e = cudaStreamEndCapture(g, &graph);
+        if (st != PN_OK) return st;
+        PN_CUDA(e);
+        PN_CUDA(cudaGraphInstantiate(&c->gexec, graph, 0));
+        cudaGraphDestroy(graph);
+        c->graph_launches = c->launches - l0;
+        c->launches = l0;
+        c->gkey = key;
+    }
+    long long issued = 0;
+    while (true) {
+        PN_CUDA(cudaGraphLaunch(c->gexec, g));
+        c->launches += c->graph_launches;
+        issued += gb;
+        PN_CUDA(cudaMemcpyAsync(c->h_state, c->state, sizeof(State), cudaMemcpyDeviceToHost, g));
+        PN_CUDA(cudaStreamSynchronize(g));
+        if (c->h_state->done || issued >= o->max_iter) break;
+    }
+    PN_CUDA(cudaEventRecord(c->gev1, g));
+    PN_CUDA(cudaStreamWaitEvent(s, c->gev1, 0));
     return PN_OK;
 }
 
@@ -500,18 +552,25 @@ static int solve_group(std::vector<pn_context *> &cs, const pn_solve_opts *o, co
     PN_TRY(group_vec(cs, V_COPY, &pn_context::p, ZT, nullptr, false, s));
     PN_TRY(group_dot(cs, &pn_context::z, ZT, 2, F, o, false, s));
     PN_TRY(group_scalar(cs, S_RHO, F, o, s));
-    // iterate in batches; the host polls the device stop flag between them
+    // iterate in batches; the host polls the device stop flag between them.
+    // Single-context solves replay a captured CUDA graph of `gb` iterations
+    // (kernels past the stop are predicated no-ops).
     if (o->max_iter > 0) {
-        long long batch = o->check_every > 0 ? o->check_every : 4;
-        long long issued = 0;
-        while (true) {
-            long long n = std::min<long long>(batch, o->max_iter - issued);
-            for (long long k = 0; k < n; ++k) PN_TRY(iteration(cs, o, jacobi, seg, s));
-            issued += n;
-            PN_CUDA(cudaMemcpyAsync(c0->h_state, c0->state, sizeof(State), cudaMemcpyDeviceToHost, s));
-            PN_CUDA(cudaStreamSynchronize(s));
-            if (c0->h_state->done || issued >= o->max_iter) break;
-            if (o->check_every <= 0) batch = std::min<long long>(batch * 2, 64);
+        const bool graph = cs.size() == 1 && c0->world <= 1 && o->check_every >= 0;
+        if (graph) {
+            PN_TRY(run_graph_batches(c0, o, jacobi, seg, s));
+        } else {
+            long long batch = o->check_every > 0 ? o->check_every : 4;
+            long long issued = 0;
+            while (true) {
+                long long n = std::min<long long>(batch, o->max_iter - issued);
+                for (long long k = 0; k < n; ++k) PN_TRY(iteration(cs, o, jacobi, seg, s));
+                issued += n;
+                PN_CUDA(cudaMemcpyAsync(c0->h_state, c0->state, sizeof(State), cudaMemcpyDeviceToHost, s));
+                PN_CUDA(cudaStreamSynchronize(s));
+                if (c0->h_state->done || issued >= o->max_iter) break;
+                if (o->check_every <= 0) batch = std::min<long long>(batch * 2, 64);
+            }
         }
     }
     // true residuals (solver.py:254-255)
