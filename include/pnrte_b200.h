@@ -68,6 +68,13 @@ typedef struct {
 } pn_desc;
 
 int pn_create(const pn_desc *desc, pn_context **out);
+
+/* Generic sparse system (any SparseSystem.A, solver.py:189 accepts them):
+ * host CSR arrays (scipy layout), copied to the device; A^T is built on the
+ * device in A.T.tocsr() order.  Usable with pn_apply / pn_jacobi_diag /
+ * pn_solve (b required); stencil-only entry points return PN_ERR_UNSUPPORTED. */
+int pn_create_csr(int64_t n, int64_t nnz, const int64_t *indptr, const int32_t *indices, const double *data,
+                  int32_t device, pn_context **out);
 int pn_destroy(pn_context *ctx);
 const char *pn_last_error(void);
 

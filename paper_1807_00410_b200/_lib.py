@@ -71,6 +71,7 @@ def load():
     L.pn_kernel_launches.argtypes = [P]
     for name, args in {
         "pn_create": [ctypes.POINTER(Desc), ctypes.POINTER(P)],
+        "pn_create_csr": [I64, I64, P, P, P, I32, ctypes.POINTER(P)],
         "pn_destroy": [P],
         "pn_set_field": [P, I32, I32, F64, P, P],
         "pn_setup": [P, P],

@@ -70,6 +70,14 @@ constexpr int RED_SLOTS = 4;   // 0: ww / zzt, 1: zz, 2: rr, 3: spare
 
 struct Comm;   // halo + partial exchange (NCCL or loopback)
 
+// generic CSR operator (pn_csr.cu): A as given, A^T as A.T.tocsr()
+struct CsrOp {
+    long long n = 0, nnz = 0;
+    long long *ap = nullptr, *tp = nullptr;
+    int *aj = nullptr, *tj = nullptr;
+    double *ax = nullptr, *tx = nullptr;
+};
+
 // ------------------------------------------------------------- context --
 struct Buf {
     double *alloc = nullptr;  // includes one halo plane each side
@@ -137,6 +145,10 @@ struct pn_context {
     pn::Buf bs;                   // RHS in the solve layout
     std::vector<double> h_aw, h_tw;
 
+    // generic CSR system instead of a stencil (pn_create_csr)
+    bool is_csr = false;
+    pn::CsrOp csr;
+
     long long R_l() const { return (long long)g.nzl * g.plane; }
     long long nvox_l() const { return (long long)g.nzl * g.pvox; }
 };
@@ -160,6 +172,12 @@ int launch_dot(pn_context *c, const double *a, const double *b, int slot, cudaSt
 int launch_ddot_emul(pn_context *c, const double *a, const double *b, long long n, int slot, int threads,
                      int kernel, cudaStream_t s, bool gated = false);
 int launch_unstagger(pn_context *c, const double *u, double *out, cudaStream_t s);
+
+// generic CSR (pn_csr.cu)
+int csr_build(pn_context *c, long long n, long long nnz, const long long *ap, const int *aj, const double *ax);
+void csr_release(pn_context *c);
+int launch_csr_apply(pn_context *c, int trans, int faithful, int squared, const double *x, double *y, int red,
+                     const double *minv, double *zt, cudaStream_t s, bool gated);
 
 // elementwise ops, see pn_kernels.cu for the op codes
 int launch_vec(pn_context *c, int op, double *y, const double *a, const double *b, cudaStream_t s,

@@ -240,6 +240,40 @@ int pn_create(const pn_desc *d, pn_context **out) {
     return PN_OK;
 }
 
+int pn_create_csr(int64_t n, int64_t nnz, const int64_t *indptr, const int32_t *indices, const double *data,
+                  int32_t device, pn_context **out) {
+    if (!out || n < 1 || nnz < 0 || !indptr || (nnz && (!indices || !data))) {
+        set_error("invalid CSR arguments");
+        return PN_ERR_INVALID;
+    }
+    if (indptr[0] != 0 || indptr[n] != nnz) { set_error("indptr does not span nnz"); return PN_ERR_INVALID; }
+    for (int64_t e = 0; e < nnz; ++e)
+        if (indices[e] < 0 || indices[e] >= n) { set_error("column index out of range"); return PN_ERR_INVALID; }
+    PN_CUDA(cudaSetDevice(device));
+    pn_context *c = new pn_context();
+    c->is_csr = true;
+    c->device = device;
+    c->U = 1;
+    Geo &g = c->g;
+    g.U = 1; g.nx = (int)n; g.ny = 1; g.nz = 1; g.z0 = 0; g.nzl = 1;
+    g.pvox = n;
+    g.plane = n;
+    int st = csr_build(c, n, nnz, (const long long *)indptr, indices, data);
+    if (st == PN_OK) {
+        c->red_bx = (int)std::max<long long>(1, std::min<long long>((n + 255) / 256, 2 * 148 * 8));
+        st = dalloc(c, &c->partials, (size_t)RED_SLOTS * c->red_bx);
+    }
+    if (st == PN_OK) st = dalloc(c, &c->plane_sums, RED_SLOTS);
+    if (st == PN_OK) st = dalloc(c, &c->ddot_chunks, 4 * 64);
+    if (st == PN_OK) st = dalloc(c, &c->state, 1);
+    if (st == PN_OK) st = alloc_buf(c, c->b);
+    if (st == PN_OK && cudaMallocHost(&c->h_state, sizeof(State)) != cudaSuccess) st = PN_ERR_NOMEM;
+    if (st != PN_OK) { pn_destroy(c); return st; }
+    c->setup_done = true;
+    *out = c;
+    return PN_OK;
+}
+
 int pn_destroy(pn_context *c) {
     if (!c) return PN_OK;
     cudaSetDevice(c->device);
@@ -250,38 +284,36 @@ int pn_destroy(pn_context *c) {
     if (c->gev1) cudaEventDestroy(c->gev1);
     if (c->gstream) cudaStreamDestroy(c->gstream);
     for (void *p : c->dev_allocs) cudaFree(p);
-    for (double *p : c->field_alloc) cudaFree(p);
+    for (double *p : c->field_alloc)
+        if (p) cudaFree(p);
     if (c->h_state) cudaFreeHost(c->h_state);
     pn_seg_release(c);
+    if (c->is_csr) csr_release(c);
     delete c;
     return PN_OK;
 }
 
 int pn_set_field(pn_context *c, int32_t slot, int32_t kind, double scalar, const double *data, void *stream) {
+    if (c && c->is_csr) { set_error("not available for a generic CSR system"); return PN_ERR_UNSUPPORTED; }
     if (!c || slot < 0 || slot >= c->n_fields) { set_error("bad field slot"); return PN_ERR_INVALID; }
     cudaStream_t s = (cudaStream_t)stream;
     PN_CUDA(cudaSetDevice(c->device));
     c->f.kind[slot] = kind;
     c->f.scalar[slot] = scalar;
     c->f.data[slot] = nullptr;
-    if (kind == 1 && slot < 2) {
-        // sigma_t / sigma_s are read as arrays by the fast kernels
-        double *dst;
+    if ((kind == 1 && slot < 2) || kind == 2) {
+        if (kind == 2 && !data) { set_error("array field without data"); return PN_ERR_INVALID; }
+        // one slab buffer per slot, reused when the field is set again
+        if ((int)c->field_alloc.size() < c->n_fields) c->field_alloc.resize(c->n_fields, nullptr);
+        double *&dst = c->field_alloc[slot];
         size_t n = (size_t)(c->g.nzl + 1) * c->g.pvox;
-        cudaError_t e = cudaMalloc(&dst, n * sizeof(double));
-        if (e != cudaSuccess) { set_error(cudaGetErrorString(e)); return PN_ERR_NOMEM; }
-        c->field_alloc.push_back(dst);
-        PN_TRY(launch_fill(dst, (long long)n, scalar, s));
+        if (!dst) {
+            cudaError_t e = cudaMalloc(&dst, n * sizeof(double));
+            if (e != cudaSuccess) { dst = nullptr; set_error(cudaGetErrorString(e)); return PN_ERR_NOMEM; }
+        }
+        if (kind == 1) PN_TRY(launch_fill(dst, (long long)n, scalar, s));   // sigma read as arrays by fast kernels
+        else PN_TRY(launch_field_slab(c, slot, data, dst, s));
         c->f.kind[slot] = 2;
-        c->f.data[slot] = dst;
-    } else if (kind == 2) {
-        if (!data) { set_error("array field without data"); return PN_ERR_INVALID; }
-        double *dst;
-        size_t n = (size_t)(c->g.nzl + 1) * c->g.pvox;
-        cudaError_t e = cudaMalloc(&dst, n * sizeof(double));
-        if (e != cudaSuccess) { set_error(cudaGetErrorString(e)); return PN_ERR_NOMEM; }
-        c->field_alloc.push_back(dst);
-        PN_TRY(launch_field_slab(c, slot, data, dst, s));
         c->f.data[slot] = dst;
     }
     c->setup_done = false;
@@ -290,6 +322,7 @@ int pn_set_field(pn_context *c, int32_t slot, int32_t kind, double scalar, const
 }
 
 int pn_setup(pn_context *c, void *stream) {
+    if (c && c->is_csr) { set_error("not available for a generic CSR system"); return PN_ERR_UNSUPPORTED; }
     cudaStream_t s = (cudaStream_t)stream;
     PN_CUDA(cudaSetDevice(c->device));
     // lambda_l * p_l per comp when every phase field is uniform (fast diagonal)
@@ -316,6 +349,7 @@ int pn_setup(pn_context *c, void *stream) {
 }
 
 int pn_export_diag_rhs(pn_context *c, double *diag, double *rhs, void *stream) {
+    if (c && c->is_csr) { set_error("not available for a generic CSR system"); return PN_ERR_UNSUPPORTED; }
     cudaStream_t s = (cudaStream_t)stream;
     if (!c->setup_done) { set_error("pn_setup not called"); return PN_ERR_INVALID; }
     if (diag) PN_TRY(ensure_diag(c, s));
@@ -330,6 +364,13 @@ int64_t pn_kernel_launches(pn_context *c) { return c ? c->launches : 0; }
 }  // extern "C"
 
 namespace pn {
+
+// colsum(A o A) as A^T-with-squared-entries applied to ones, ascending row order
+static int squared_transpose_apply(pn_context *c, const double *ones, double *out, cudaStream_t s) {
+    if (c->is_csr) return launch_csr_apply(c, 1, 1, 1, ones, out, 0, nullptr, nullptr, s, false);
+    PN_TRY(ensure_diag(c, s));
+    return launch_apply_faithful(c, 1, 1, ones, out, s, false);
+}
 
 static int ensure_vectors(pn_context *c, bool jacobi) {
     for (Buf *b : {&c->x, &c->r, &c->p, &c->z, &c->w, &c->tmp}) PN_TRY(alloc_buf(c, *b));
@@ -346,9 +387,14 @@ static int group_apply(std::vector<pn_context *> &cs, int trans, int faithful, B
                        Buf pn_context::*out, int red, bool jacobi, bool gated, cudaStream_t s, bool seg = false) {
     PN_TRY(halo_exchange(cs, in, s));
     for (auto *c : cs) {
-        if (faithful || !(c->canonical_diag && c->uniform_phase)) PN_TRY(ensure_diag(c, s));
         const double *x = (c->*in).p;
         double *y = (c->*out).p;
+        if (c->is_csr) {
+            PN_TRY(launch_csr_apply(c, trans, faithful, 0, x, y, faithful ? 0 : red, jacobi ? c->minv.p : nullptr,
+                                    jacobi ? c->zt.p : nullptr, s, gated));
+            continue;
+        }
+        if (faithful || !(c->canonical_diag && c->uniform_phase)) PN_TRY(ensure_diag(c, s));
         if (faithful) {
             PN_TRY(launch_apply_faithful(c, trans, 0, x, y, s, gated));
         } else if (seg) {
@@ -508,6 +554,8 @@ static int solve_group(std::vector<pn_context *> &cs, const pn_solve_opts *o, co
         h.max_iter = o->max_iter;
         PN_CUDA(cudaMemcpyAsync(c->state, &h, sizeof(State), cudaMemcpyHostToDevice, s));
     }
+    for (size_t i = 0; i < cs.size(); ++i)
+        if (cs[i]->is_csr && !(bs && bs[i])) { set_error("a CSR system needs its right-hand side"); return PN_ERR_INVALID; }
     // b (caller RHS or the assembled Q) in the solve layout
     for (size_t i = 0; i < cs.size(); ++i)
         PN_TRY(to_solve_layout(cs[i], seg, (bs && bs[i]) ? bs[i] : cs[i]->b.p, cs[i]->bs.p, s));
@@ -532,10 +580,7 @@ static int solve_group(std::vector<pn_context *> &cs, const pn_solve_opts *o, co
         // minv = 1 / colsum(A o A), 0 -> 1 (solver.py:218-223), exact order, then solve layout
         PN_TRY(group_vec(cs, V_FILL_ONE, &pn_context::tmp, nullptr, nullptr, false, s));
         PN_TRY(halo_exchange(cs, &pn_context::tmp, s));
-        for (auto *c : cs) {
-            PN_TRY(ensure_diag(c, s));
-            PN_TRY(launch_apply_faithful(c, 1, 1, c->tmp.p, c->w.p, s, false));
-        }
+        for (auto *c : cs) PN_TRY(squared_transpose_apply(c, c->tmp.p, c->w.p, s));
         PN_TRY(group_vec(cs, V_RECIP_DIAG, &pn_context::tmp, &pn_context::w, nullptr, false, s));
         for (auto *c : cs) PN_TRY(to_solve_layout(c, seg, c->tmp.p, c->minv.p, s));
     }
@@ -628,11 +673,9 @@ int pn_jacobi_diag(pn_context *c, double *out, void *stream) {
     if (!c->setup_done) { set_error("pn_setup not called"); return PN_ERR_INVALID; }
     PN_TRY(alloc_buf(c, c->tmp));
     std::vector<pn_context *> cs{c};
-    PN_TRY(ensure_diag(c, s));
     PN_TRY(group_vec(cs, V_FILL_ONE, &pn_context::tmp, nullptr, nullptr, false, s));
     PN_TRY(halo_exchange(cs, &pn_context::tmp, s));
-    PN_TRY(launch_apply_faithful(c, 1, 1, c->tmp.p, out, s, false));
-    return PN_OK;
+    return squared_transpose_apply(c, c->tmp.p, out, s);
 }
 
 int pn_solve(pn_context *c, const pn_solve_opts *o, const double *b, const double *x0, double *x, pn_report *rep,
@@ -651,6 +694,7 @@ int pn_group_solve(pn_context **ctxs, int32_t n, const pn_solve_opts *o, double 
 }
 
 int pn_unstagger(pn_context *c, const double *u, double *out, void *stream) {
+    if (c && c->is_csr) { set_error("not available for a generic CSR system"); return PN_ERR_UNSUPPORTED; }
     cudaStream_t s = (cudaStream_t)stream;
     PN_TRY(alloc_buf(c, c->tmp));
     PN_CUDA(cudaMemcpyAsync(c->tmp.p, u, c->R_l() * sizeof(double), cudaMemcpyDeviceToDevice, s));

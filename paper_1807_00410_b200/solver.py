@@ -132,6 +132,36 @@ class PnContext:
         self._L = L
         self._torch = torch
 
+    @classmethod
+    def from_csr(cls, A, device=0):
+        """Device context of a generic sparse system (any SparseSystem.A)."""
+        import scipy.sparse as sp
+        torch = _torch()
+        L = _lib.load()
+        A = sp.csr_matrix(A)
+        if A.shape[0] != A.shape[1]:
+            raise ValueError("system matrix must be square")
+        indptr = np.ascontiguousarray(A.indptr, dtype=np.int64)
+        indices = np.ascontiguousarray(A.indices, dtype=np.int32)
+        data = np.ascontiguousarray(A.data, dtype=np.float64)
+        self = cls.__new__(cls)
+        self.tables = None
+        self.N, self.U = 0, 1
+        self.res = (A.shape[0], 1, 1)
+        self.h = 1.0
+        self.device = int(device)
+        self.z0, self.nz_local = 0, 1
+        self.R_local = A.shape[0]
+        self.pk = None
+        handle = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            _lib.check(L.pn_create_csr(A.shape[0], len(data), indptr.ctypes.data, indices.ctypes.data,
+                                       data.ctypes.data, self.device, ctypes.byref(handle)))
+        self.handle = handle
+        self._L = L
+        self._torch = torch
+        return self
+
     def __del__(self):
         h = getattr(self, "handle", None)
         if h is not None and h.value:
@@ -332,9 +362,12 @@ def solve_normal_cg(system, tol=1e-8, max_iter=50000, primal_tol=None, jacobi=Fa
     if tol <= 0:
         raise ValueError("tolerance must be positive")
     A = system.A
-    if not isinstance(A, StencilOperator):
-        raise NotImplementedError("generic CSR systems: use a stencil system from assemble()")
-    ctx = A.ctx
+    if isinstance(A, StencilOperator):
+        ctx = A.ctx
+    else:
+        # any sparse system (the reference's SparseSystem with a scipy matrix):
+        # device CSR operator, same CGNR driver
+        ctx = PnContext.from_csr(A)
     b = None
     t0 = time.perf_counter()
     x, rep = ctx.solve(tol=tol, max_iter=max_iter, primal_tol=primal_tol, jacobi=jacobi, x0=x0, b=system.Q

@@ -184,3 +184,67 @@ def test_loopback_slabs_match_single_slab(N, res, slabs):
     _lib.check(L.pn_group_solve(hs, slabs, ctypes.byref(opts), xp, ctypes.byref(rep), None, None, 0, None))
     assert rep.iterations == ro.iterations
     assert torch.equal(torch.cat(xs), xo)
+
+
+# ---------------------------------------------------------------------------
+# generic CSR systems (test_solver.py:99-145 of the reference)
+# ---------------------------------------------------------------------------
+
+def _csr_system(A, b):
+    import scipy.sparse as sp
+    from paper_1807_00410_b200.solver import SparseSystem
+    return SparseSystem(A=sp.csr_matrix(A), Q=b, res=(len(b),), n_unknowns=1)
+
+
+def test_csr_identity_single_iteration():
+    import scipy.sparse as sp
+    from paper_1807_00410_b200.solver import solve_normal_cg
+    b = np.zeros(6)
+    b[0] = 1.0
+    x, rep = solve_normal_cg(_csr_system(sp.identity(6, format="csr"), b), tol=1e-12)
+    np.testing.assert_allclose(x, b, atol=1e-12)
+    assert rep.converged and rep.iterations == 1
+
+
+def test_csr_matches_dense_lu():
+    from paper_1807_00410_b200.solver import solve_normal_cg
+    rng = np.random.default_rng(1)
+    n = 50
+    A = rng.normal(size=(n, n)) + n * np.eye(n)
+    b = A @ rng.normal(size=n)
+    x, rep = solve_normal_cg(_csr_system(A, b), tol=1e-12, max_iter=2000)
+    assert rep.converged
+    np.testing.assert_allclose(x, np.linalg.solve(A, b), atol=1e-8)
+
+
+def test_csr_nonconvergence_and_jacobi():
+    from paper_1807_00410_b200.solver import solve_normal_cg
+    rng = np.random.default_rng(2)
+    A = rng.normal(size=(40, 40)) + np.diag(np.logspace(0, 6, 40))
+    _, rep = solve_normal_cg(_csr_system(A, rng.normal(size=40)), tol=1e-14, max_iter=3)
+    assert not rep.converged and rep.iterations == 3 and len(rep.normal_history) == 3
+    rng = np.random.default_rng(3)
+    A = rng.normal(size=(60, 60)) + np.diag(rng.uniform(5, 500, 60))
+    b = rng.normal(size=60)
+    x0, r0 = solve_normal_cg(_csr_system(A, b), tol=1e-12, max_iter=5000)
+    x1, r1 = solve_normal_cg(_csr_system(A, b), tol=1e-12, max_iter=5000, jacobi=True)
+    assert r0.converged and r1.converged
+    np.testing.assert_allclose(x0, x1, atol=1e-6)
+
+
+@pytest.mark.parametrize("case", ["p3_456", "p7_343", "p1_3286"])
+@pytest.mark.parametrize("jac", [0, 1])
+def test_csr_faithful_bit_identical_to_reference(case, jac, golden):
+    """The reference's own assembled CSR (fixture), solved on the device in
+    faithful mode: bit-identical to solve_normal_cg on that matrix."""
+    import scipy.sparse as sp
+    from paper_1807_00410_b200.solver import SparseSystem, solve_normal_cg
+    g, meta = golden["cases"], golden["cases_meta"]["cases"][case]
+    n = len(g[f"{case}/indptr"]) - 1
+    A = sp.csr_matrix((g[f"{case}/data"], g[f"{case}/indices"], g[f"{case}/indptr"]), shape=(n, n))
+    s = SparseSystem(A=A, Q=g[f"{case}/Q"], res=(n,), n_unknowns=1)
+    x, rep = solve_normal_cg(s, tol=1e-9, max_iter=400, jacobi=bool(jac), mode="faithful", blas_threads=8,
+                             blas_kernel=0)
+    assert rep.iterations == meta[f"cg{jac}"]["iterations"]
+    assert x.tobytes() == g[f"{case}/cg{jac}/x"].tobytes()
+    assert np.array(rep.normal_history).tobytes() == g[f"{case}/cg{jac}/nh"].tobytes()
