@@ -133,6 +133,10 @@ struct pn_context {
 
     long long launches = 0;
 
+    // multi-slab: halo exchange on its own stream, overlapped with interior planes
+    cudaStream_t comm_stream = nullptr;
+    cudaEvent_t cev_ready = nullptr, cev_halo = nullptr;
+
     // CUDA graph of a batch of CGNR iterations (single context, no NCCL)
     cudaStream_t gstream = nullptr;
     cudaEvent_t gev0 = nullptr, gev1 = nullptr;
@@ -160,7 +164,7 @@ int launch_fill(double *p, long long n, double v, cudaStream_t s);
 int launch_field_slab(pn_context *c, int slot, const double *src, double *dst, cudaStream_t s);
 int launch_setup(pn_context *c, bool want_diag, bool want_rhs, cudaStream_t s);
 int launch_apply_table(pn_context *c, int trans, int faithful, int squared, const double *x, double *y, int red,
-                       const double *minv, double *zt, cudaStream_t s, bool gated);
+                       const double *minv, double *zt, cudaStream_t s, bool gated, int kl0 = 0, int npl = -1);
 int launch_apply_faithful(pn_context *c, int trans, int squared, const double *x, double *y,
                           cudaStream_t s, bool gated = false);
 int launch_xr(pn_context *c, cudaStream_t s);

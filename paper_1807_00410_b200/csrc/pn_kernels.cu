@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(256) k_apply_table(Tables T, Fields F, Geo g, 
                                                      const double *__restrict__ x, double *__restrict__ y,
                                                      const double *__restrict__ diag, int red, const double *minv,
                                                      double *zt, double *partials, long long slot_stride, int rb,
-                                                     const State *st) {
+                                                     const State *st, int kl0) {
     if (st && stopped(st)) return;
     extern __shared__ unsigned char smem_raw[];
     const int U = g.U;
@@ -188,7 +188,7 @@ __global__ void __launch_bounds__(256) k_apply_table(Tables T, Fields F, Geo g, 
         for (int e = threadIdx.x; e < U; e += blockDim.x) { spar[e] = T.par[e]; slamp[e] = T.lamp[e]; }
     }
     __syncthreads();
-    const int kl = blockIdx.y;
+    const int kl = kl0 + blockIdx.y;
     const long long chunk = (g.plane + rb - 1) / rb;
     const long long r0 = (long long)blockIdx.x * chunk;
     const long long r1 = min(g.plane, r0 + chunk);
@@ -273,21 +273,23 @@ static size_t table_smem(const pn_context *c, int trans) {
 static long long slot_stride(const pn_context *c) { return (long long)c->g.nz * c->red_bx; }
 
 int launch_apply_table(pn_context *c, int trans, int faithful, int squared, const double *x, double *y, int red,
-                       const double *minv, double *zt, cudaStream_t s, bool gated) {
-    dim3 grid(c->red_bx, c->g.nzl);
+                       const double *minv, double *zt, cudaStream_t s, bool gated, int kl0, int npl) {
+    if (npl < 0) npl = c->g.nzl;
+    if (npl <= 0) return PN_OK;
+    dim3 grid(c->red_bx, npl);
     size_t sm = table_smem(c, trans);
     const State *st = gated ? c->state : nullptr;
     bool recompute = !faithful && c->canonical_diag && c->uniform_phase;
     if (!recompute && !c->diag_ready) { set_error("internal: diagonal not assembled"); return PN_ERR_INVALID; }
     if (faithful) {
         k_apply_table<true, false><<<grid, 256, sm, s>>>(c->tb, c->f, c->g, trans, squared, x, y, c->diag, red, minv,
-                                                         zt, c->partials, slot_stride(c), c->red_bx, st);
+                                                         zt, c->partials, slot_stride(c), c->red_bx, st, kl0);
     } else if (recompute) {
         k_apply_table<false, true><<<grid, 256, sm, s>>>(c->tb, c->f, c->g, trans, 0, x, y, c->diag, red, minv, zt,
-                                                         c->partials, slot_stride(c), c->red_bx, st);
+                                                         c->partials, slot_stride(c), c->red_bx, st, kl0);
     } else {
         k_apply_table<false, false><<<grid, 256, sm, s>>>(c->tb, c->f, c->g, trans, 0, x, y, c->diag, red, minv, zt,
-                                                          c->partials, slot_stride(c), c->red_bx, st);
+                                                          c->partials, slot_stride(c), c->red_bx, st, kl0);
     }
     PN_CUDA(cudaGetLastError());
     c->launches++;
@@ -296,7 +298,7 @@ int launch_apply_table(pn_context *c, int trans, int faithful, int squared, cons
 
 int launch_apply_faithful(pn_context *c, int trans, int squared, const double *x, double *y, cudaStream_t s,
                           bool gated) {
-    return launch_apply_table(c, trans, 1, squared, x, y, 0, nullptr, nullptr, s, gated);
+    return launch_apply_table(c, trans, 1, squared, x, y, 0, nullptr, nullptr, s, gated, 0, -1);
 }
 
 // ----------------------------------------------------------- vector ops --

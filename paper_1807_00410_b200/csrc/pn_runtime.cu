@@ -282,6 +282,9 @@ int pn_destroy(pn_context *c) {
     if (c->gexec) cudaGraphExecDestroy(c->gexec);
     if (c->gev0) cudaEventDestroy(c->gev0);
     if (c->gev1) cudaEventDestroy(c->gev1);
+    if (c->cev_ready) cudaEventDestroy(c->cev_ready);
+    if (c->cev_halo) cudaEventDestroy(c->cev_halo);
+    if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
     if (c->gstream) cudaStreamDestroy(c->gstream);
     for (void *p : c->dev_allocs) cudaFree(p);
     for (double *p : c->field_alloc)
@@ -381,27 +384,54 @@ static int ensure_vectors(pn_context *c, bool jacobi) {
     return PN_OK;
 }
 
+// apply of local planes [kl0, kl0+npl) of one context
+static int apply_planes(pn_context *c, int trans, int faithful, const double *x, double *y, int red, bool jacobi,
+                        bool gated, cudaStream_t s, bool seg, int kl0, int npl) {
+    if (c->is_csr)
+        return launch_csr_apply(c, trans, faithful, 0, x, y, faithful ? 0 : red, jacobi ? c->minv.p : nullptr,
+                                jacobi ? c->zt.p : nullptr, s, gated);
+    if (faithful || !(c->canonical_diag && c->uniform_phase)) PN_TRY(ensure_diag(c, s));
+    if (faithful) return launch_apply_table(c, trans, 1, 0, x, y, 0, nullptr, nullptr, s, gated, kl0, npl);
+    if (seg)
+        return pn_seg_apply(c, trans, x, y, red, jacobi ? c->minv.p : nullptr, jacobi ? c->zt.p : nullptr, gated, s,
+                            kl0, npl);
+    return launch_apply_table(c, trans, 0, 0, x, y, red, jacobi ? c->minv.p : nullptr, jacobi ? c->zt.p : nullptr, s,
+                              gated, kl0, npl);
+}
+
 // one operator apply on padded internal vectors of a slab group
-// red: 0 none, 1 ww -> slot 0, 2 z/zt -> slots 1,2
+// red: 0 none, 1 ww -> slot 0, 2 z/zt -> slots 1,2.
+// Multi-slab: the halo exchange runs on a side stream while the interior
+// planes (which do not read halos) compute; the two boundary planes follow.
 static int group_apply(std::vector<pn_context *> &cs, int trans, int faithful, Buf pn_context::*in,
                        Buf pn_context::*out, int red, bool jacobi, bool gated, cudaStream_t s, bool seg = false) {
-    PN_TRY(halo_exchange(cs, in, s));
-    for (auto *c : cs) {
-        const double *x = (c->*in).p;
-        double *y = (c->*out).p;
-        if (c->is_csr) {
-            PN_TRY(launch_csr_apply(c, trans, faithful, 0, x, y, faithful ? 0 : red, jacobi ? c->minv.p : nullptr,
-                                    jacobi ? c->zt.p : nullptr, s, gated));
-            continue;
+    pn_context *c0 = cs[0];
+    if (c0->world <= 1 || c0->is_csr) {
+        for (auto *c : cs)
+            PN_TRY(apply_planes(c, trans, faithful, (c->*in).p, (c->*out).p, red, jacobi, gated, s, seg, 0, -1));
+    } else {
+        if (!c0->comm_stream) {
+            PN_CUDA(cudaStreamCreateWithFlags(&c0->comm_stream, cudaStreamNonBlocking));
+            PN_CUDA(cudaEventCreateWithFlags(&c0->cev_ready, cudaEventDisableTiming));
+            PN_CUDA(cudaEventCreateWithFlags(&c0->cev_halo, cudaEventDisableTiming));
         }
-        if (faithful || !(c->canonical_diag && c->uniform_phase)) PN_TRY(ensure_diag(c, s));
-        if (faithful) {
-            PN_TRY(launch_apply_faithful(c, trans, 0, x, y, s, gated));
-        } else if (seg) {
-            PN_TRY(pn_seg_apply(c, trans, x, y, red, jacobi ? c->minv.p : nullptr, jacobi ? c->zt.p : nullptr, gated, s));
-        } else {
-            PN_TRY(launch_apply_table(c, trans, 0, 0, x, y, red, jacobi ? c->minv.p : nullptr,
-                                      jacobi ? c->zt.p : nullptr, s, gated));
+        PN_CUDA(cudaEventRecord(c0->cev_ready, s));
+        PN_CUDA(cudaStreamWaitEvent(c0->comm_stream, c0->cev_ready, 0));
+        PN_TRY(halo_exchange(cs, in, c0->comm_stream));
+        PN_CUDA(cudaEventRecord(c0->cev_halo, c0->comm_stream));
+        for (auto *c : cs) {
+            const int nzl = c->g.nzl;
+            if (nzl > 2)
+                PN_TRY(apply_planes(c, trans, faithful, (c->*in).p, (c->*out).p, red, jacobi, gated, s, seg, 1,
+                                    nzl - 2));
+        }
+        PN_CUDA(cudaStreamWaitEvent(s, c0->cev_halo, 0));
+        for (auto *c : cs) {
+            const int nzl = c->g.nzl;
+            PN_TRY(apply_planes(c, trans, faithful, (c->*in).p, (c->*out).p, red, jacobi, gated, s, seg, 0, 1));
+            if (nzl > 1)
+                PN_TRY(apply_planes(c, trans, faithful, (c->*in).p, (c->*out).p, red, jacobi, gated, s, seg, nzl - 1,
+                                    1));
         }
     }
     if (red == 1) PN_TRY(gather_partials(cs, 1, s));

@@ -75,8 +75,12 @@ int pn_seg_prepare(pn_context *c, cudaStream_t) {
 }
 
 int pn_seg_apply(pn_context *c, int trans, const double *x, double *y, int red, const double *minv, double *zt,
-                 bool gated, cudaStream_t s) {
+                 bool gated, cudaStream_t s, int kl0, int npl) {
     SegCtx *sc = (SegCtx *)c->seg;
+    SegGeo g = sc->g;
+    g.kl0 = kl0;
+    g.npl = npl < 0 ? c->g.nzl : npl;
+    if (g.npl <= 0) return PN_OK;
     const SegParams &prm = trans ? *sc->pt : *sc->pa;
     const long long stride = (long long)c->g.nz * c->red_bx;
     const State *st = gated ? c->state : nullptr;
@@ -85,7 +89,7 @@ int pn_seg_apply(pn_context *c, int trans, const double *x, double *y, int red, 
     switch (c->N) {
 #define PN_N(n)                                                                                                 \
     case n:                                                                                                     \
-        rc = seg_launch<n>(prm, sc->g, trans, red, minv != nullptr, x, y, minv, zt, sig_t, sig_s, c->partials, \
+        rc = seg_launch<n>(prm, g, trans, red, minv != nullptr, x, y, minv, zt, sig_t, sig_s, c->partials, \
                            stride, c->red_bx, st, s);                                                           \
         break;
         PN_N(1) PN_N(2) PN_N(3) PN_N(4) PN_N(5) PN_N(6) PN_N(7)

@@ -181,8 +181,8 @@ __global__ void __launch_bounds__(SegTune<N>::threads, SegTune<N>::minb) k_seg(
     const int tyb = min(g.tyb, g.nyb);
     const int jb_in = (int)(bid % tyb);
     bid /= tyb;
-    const int kl = (int)(bid % g.nzl);
-    const int jb = (int)(bid / g.nzl) * tyb + jb_in;
+    const int kl = g.kl0 + (int)(bid % g.npl);
+    const int jb = (int)(bid / g.npl) * tyb + jb_in;
     const int j = jb < g.nyb ? jb * SegTune<N>::rows + rw : g.ny;
     const int kg = g.z0 + kl;
     constexpr long long rowlen = (long long)U * 32;
@@ -292,7 +292,7 @@ int seg_launch(const SegParams &prm, const SegGeo &g, int trans, int red, bool j
                long long slot_stride, int rb, const State *state, cudaStream_t s) {
     constexpr int rows = SegTune<N>::rows;
     const long long ytiles = (g.nyb + g.tyb - 1) / g.tyb;
-    dim3 grid((unsigned)((long long)g.nseg * g.tyb * g.nzl * ytiles)), block(SegTune<N>::threads);
+    dim3 grid((unsigned)((long long)g.nseg * g.tyb * g.npl * ytiles)), block(SegTune<N>::threads);
     const size_t smem = rows * seg_smem_per_warp<N>();
     if (g.nyb != (g.ny + rows - 1) / rows) { set_error("segmented launch: row blocking mismatch"); return PN_ERR_INVALID; }
 #define PN_SEG_GO(T, R, J)                                                                                   \

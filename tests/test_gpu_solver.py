@@ -148,7 +148,7 @@ def _group(tables, spec, n_slabs):
     return out
 
 
-@pytest.mark.parametrize("N,res,slabs", [(1, (32, 8, 8), 2), (3, (32, 6, 8), 4), (7, (32, 4, 4), 2),
+@pytest.mark.parametrize("N,res,slabs", [(1, (32, 8, 8), 2), (3, (32, 6, 8), 4), (7, (32, 4, 4), 2), (5, (32, 8, 12), 3), (7, (64, 8, 10), 2),
                                          (3, (7, 5, 6), 3)])
 def test_loopback_slabs_match_single_slab(N, res, slabs):
     """z-slab decomposition (halo planes + all-gathered plane partials) gives
