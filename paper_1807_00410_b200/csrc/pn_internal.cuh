@@ -164,7 +164,8 @@ int launch_fill(double *p, long long n, double v, cudaStream_t s);
 int launch_field_slab(pn_context *c, int slot, const double *src, double *dst, cudaStream_t s);
 int launch_setup(pn_context *c, bool want_diag, bool want_rhs, cudaStream_t s);
 int launch_apply_table(pn_context *c, int trans, int faithful, int squared, const double *x, double *y, int red,
-                       const double *minv, double *zt, cudaStream_t s, bool gated, int kl0 = 0, int npl = -1);
+                       const double *minv, double *zt, cudaStream_t s, bool gated, int kl0 = 0, int npl = -1,
+                       int kst = 1);
 int launch_apply_faithful(pn_context *c, int trans, int squared, const double *x, double *y,
                           cudaStream_t s, bool gated = false);
 int launch_xr(pn_context *c, cudaStream_t s);

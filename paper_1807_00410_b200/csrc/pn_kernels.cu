@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(256) k_apply_table(Tables T, Fields F, Geo g, 
                                                      const double *__restrict__ x, double *__restrict__ y,
                                                      const double *__restrict__ diag, int red, const double *minv,
                                                      double *zt, double *partials, long long slot_stride, int rb,
-                                                     const State *st, int kl0) {
+                                                     const State *st, int kl0, int kst) {
     if (st && stopped(st)) return;
     extern __shared__ unsigned char smem_raw[];
     const int U = g.U;
@@ -188,7 +188,7 @@ __global__ void __launch_bounds__(256) k_apply_table(Tables T, Fields F, Geo g, 
         for (int e = threadIdx.x; e < U; e += blockDim.x) { spar[e] = T.par[e]; slamp[e] = T.lamp[e]; }
     }
     __syncthreads();
-    const int kl = kl0 + blockIdx.y;
+    const int kl = kl0 + blockIdx.y * kst;
     const long long chunk = (g.plane + rb - 1) / rb;
     const long long r0 = (long long)blockIdx.x * chunk;
     const long long r1 = min(g.plane, r0 + chunk);
@@ -273,7 +273,7 @@ static size_t table_smem(const pn_context *c, int trans) {
 static long long slot_stride(const pn_context *c) { return (long long)c->g.nz * c->red_bx; }
 
 int launch_apply_table(pn_context *c, int trans, int faithful, int squared, const double *x, double *y, int red,
-                       const double *minv, double *zt, cudaStream_t s, bool gated, int kl0, int npl) {
+                       const double *minv, double *zt, cudaStream_t s, bool gated, int kl0, int npl, int kst) {
     if (npl < 0) npl = c->g.nzl;
     if (npl <= 0) return PN_OK;
     dim3 grid(c->red_bx, npl);
@@ -283,13 +283,13 @@ int launch_apply_table(pn_context *c, int trans, int faithful, int squared, cons
     if (!recompute && !c->diag_ready) { set_error("internal: diagonal not assembled"); return PN_ERR_INVALID; }
     if (faithful) {
         k_apply_table<true, false><<<grid, 256, sm, s>>>(c->tb, c->f, c->g, trans, squared, x, y, c->diag, red, minv,
-                                                         zt, c->partials, slot_stride(c), c->red_bx, st, kl0);
+                                                         zt, c->partials, slot_stride(c), c->red_bx, st, kl0, kst);
     } else if (recompute) {
         k_apply_table<false, true><<<grid, 256, sm, s>>>(c->tb, c->f, c->g, trans, 0, x, y, c->diag, red, minv, zt,
-                                                         c->partials, slot_stride(c), c->red_bx, st, kl0);
+                                                         c->partials, slot_stride(c), c->red_bx, st, kl0, kst);
     } else {
         k_apply_table<false, false><<<grid, 256, sm, s>>>(c->tb, c->f, c->g, trans, 0, x, y, c->diag, red, minv, zt,
-                                                          c->partials, slot_stride(c), c->red_bx, st, kl0);
+                                                          c->partials, slot_stride(c), c->red_bx, st, kl0, kst);
     }
     PN_CUDA(cudaGetLastError());
     c->launches++;
@@ -298,7 +298,7 @@ int launch_apply_table(pn_context *c, int trans, int faithful, int squared, cons
 
 int launch_apply_faithful(pn_context *c, int trans, int squared, const double *x, double *y, cudaStream_t s,
                           bool gated) {
-    return launch_apply_table(c, trans, 1, squared, x, y, 0, nullptr, nullptr, s, gated, 0, -1);
+    return launch_apply_table(c, trans, 1, squared, x, y, 0, nullptr, nullptr, s, gated, 0, -1, 1);
 }
 
 // ----------------------------------------------------------- vector ops --

@@ -386,17 +386,17 @@ static int ensure_vectors(pn_context *c, bool jacobi) {
 
 // apply of local planes [kl0, kl0+npl) of one context
 static int apply_planes(pn_context *c, int trans, int faithful, const double *x, double *y, int red, bool jacobi,
-                        bool gated, cudaStream_t s, bool seg, int kl0, int npl) {
+                        bool gated, cudaStream_t s, bool seg, int kl0, int npl, int kst = 1) {
     if (c->is_csr)
         return launch_csr_apply(c, trans, faithful, 0, x, y, faithful ? 0 : red, jacobi ? c->minv.p : nullptr,
                                 jacobi ? c->zt.p : nullptr, s, gated);
     if (faithful || !(c->canonical_diag && c->uniform_phase)) PN_TRY(ensure_diag(c, s));
-    if (faithful) return launch_apply_table(c, trans, 1, 0, x, y, 0, nullptr, nullptr, s, gated, kl0, npl);
+    if (faithful) return launch_apply_table(c, trans, 1, 0, x, y, 0, nullptr, nullptr, s, gated, kl0, npl, kst);
     if (seg)
         return pn_seg_apply(c, trans, x, y, red, jacobi ? c->minv.p : nullptr, jacobi ? c->zt.p : nullptr, gated, s,
-                            kl0, npl);
+                            kl0, npl, kst);
     return launch_apply_table(c, trans, 0, 0, x, y, red, jacobi ? c->minv.p : nullptr, jacobi ? c->zt.p : nullptr, s,
-                              gated, kl0, npl);
+                              gated, kl0, npl, kst);
 }
 
 // one operator apply on padded internal vectors of a slab group
@@ -426,12 +426,10 @@ static int group_apply(std::vector<pn_context *> &cs, int trans, int faithful, B
                                     nzl - 2));
         }
         PN_CUDA(cudaStreamWaitEvent(s, c0->cev_halo, 0));
-        for (auto *c : cs) {
+        for (auto *c : cs) {   // planes 0 and nzl-1 in one launch
             const int nzl = c->g.nzl;
-            PN_TRY(apply_planes(c, trans, faithful, (c->*in).p, (c->*out).p, red, jacobi, gated, s, seg, 0, 1));
-            if (nzl > 1)
-                PN_TRY(apply_planes(c, trans, faithful, (c->*in).p, (c->*out).p, red, jacobi, gated, s, seg, nzl - 1,
-                                    1));
+            PN_TRY(apply_planes(c, trans, faithful, (c->*in).p, (c->*out).p, red, jacobi, gated, s, seg, 0,
+                                nzl > 1 ? 2 : 1, nzl > 1 ? nzl - 1 : 1));
         }
     }
     if (red == 1) PN_TRY(gather_partials(cs, 1, s));

@@ -75,10 +75,11 @@ int pn_seg_prepare(pn_context *c, cudaStream_t) {
 }
 
 int pn_seg_apply(pn_context *c, int trans, const double *x, double *y, int red, const double *minv, double *zt,
-                 bool gated, cudaStream_t s, int kl0, int npl) {
+                 bool gated, cudaStream_t s, int kl0, int npl, int kst) {
     SegCtx *sc = (SegCtx *)c->seg;
     SegGeo g = sc->g;
     g.kl0 = kl0;
+    g.kst = kst;
     g.npl = npl < 0 ? c->g.nzl : npl;
     if (g.npl <= 0) return PN_OK;
     const SegParams &prm = trans ? *sc->pt : *sc->pa;

@@ -9,7 +9,7 @@ bool pn_seg_ok(const pn_context *c);
 int pn_seg_prepare(pn_context *c, cudaStream_t s);
 // y = A x or A^T x on segmented-layout vectors (padded, local slab)
 int pn_seg_apply(pn_context *c, int trans, const double *x, double *y, int red, const double *minv, double *zt,
-                 bool gated, cudaStream_t s, int kl0 = 0, int npl = -1);
+                 bool gated, cudaStream_t s, int kl0 = 0, int npl = -1, int kst = 1);
 // layout conversion of one local-slab vector: dir 0 = reference -> segmented, 1 = back
 int pn_seg_convert(pn_context *c, int dir, const double *src, double *dst, cudaStream_t s);
 void pn_seg_release(pn_context *c);

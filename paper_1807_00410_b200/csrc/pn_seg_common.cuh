@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(SegTune<N>::threads, SegTune<N>::minb) k_seg(
     const int tyb = min(g.tyb, g.nyb);
     const int jb_in = (int)(bid % tyb);
     bid /= tyb;
-    const int kl = g.kl0 + (int)(bid % g.npl);
+    const int kl = g.kl0 + (int)(bid % g.npl) * g.kst;
     const int jb = (int)(bid / g.npl) * tyb + jb_in;
     const int j = jb < g.nyb ? jb * SegTune<N>::rows + rw : g.ny;
     const int kg = g.z0 + kl;

@@ -26,7 +26,7 @@ struct SegParams {
 struct SegGeo {
     int U, nx, ny, nz, z0, nzl, nseg, nyb;
     int tyb;                 // row blocks per y-tile of the CTA traversal
-    int kl0, npl;            // local planes [kl0, kl0+npl) computed by one launch
+    int kl0, npl, kst;       // local planes kl0 + i*kst, i < npl, computed by one launch
     long long plane, pvox;
 };
 
