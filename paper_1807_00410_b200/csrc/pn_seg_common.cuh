@@ -25,7 +25,7 @@ namespace pn {
 struct SegRow {
     const double *xs;                       // own row staged in shared memory, + lane
     const double *eprev, *enext;            // shared: x-edge values of the adjacent segments [U]
-    const double *sig;                      // shared: sigma_t / sigma_s rows [2][4][33]
+    const double *sig;                      // shared: sigma_t / sigma_s rows [2][4][34]
     const double *Xym, *Xyp, *Xzm, *Xzp;    // neighbour rows in global memory + lane (null outside)
     double *Y;                              // output row + lane
     const double *minv;                     // Jacobi inverse diag row + lane
@@ -53,6 +53,10 @@ __device__ __forceinline__ bool pinned_yz(const SegRow &r) {
 
 __device__ __forceinline__ void cp_async16(void *dst_smem, const void *src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"((unsigned)__cvta_generic_to_shared(dst_smem)),
+                 "l"(src));
+}
+__device__ __forceinline__ void cp_async8(void *dst_smem, const void *src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"((unsigned)__cvta_generic_to_shared(dst_smem)),
                  "l"(src));
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
@@ -101,7 +105,7 @@ __device__ __forceinline__ double nb_z(const SegRow &r, int s) {
 }
 
 // average of sigma_t / sigma_s over the staggered site set of class P
-// (shared rows q = sy + 2 sz, 33 entries: 32 lanes + the x+1 sample of lane 31)
+// (shared rows q = sy + 2 sz, 34-double stride: 32 lanes + the x+1 sample of lane 31)
 template <int P>
 __device__ __forceinline__ void class_avg(const SegRow &r, double &at, double &as) {
     double t_ = 0.0, s_ = 0.0;
@@ -110,11 +114,11 @@ __device__ __forceinline__ void class_avg(const SegRow &r, double &at, double &a
 #pragma unroll
         for (int sy = 0; sy < ((P & 2) ? 2 : 1); ++sy) {
             const int q = sy + 2 * sz;
-            t_ += r.sig[q * 33];
-            s_ += r.sig[132 + q * 33];
+            t_ += r.sig[q * 34];
+            s_ += r.sig[136 + q * 34];
             if (P & 1) {
-                t_ += r.sig[q * 33 + 1];
-                s_ += r.sig[132 + q * 33 + 1];
+                t_ += r.sig[q * 34 + 1];
+                s_ += r.sig[136 + q * 34 + 1];
             }
         }
     constexpr int n = 1 << (((P >> 0) & 1) + ((P >> 1) & 1) + ((P >> 2) & 1));
@@ -160,7 +164,7 @@ template <int N> struct SegTune {
 
 template <int N>
 __host__ __device__ constexpr size_t seg_smem_per_warp() {
-    return sizeof(double) * ((size_t)32 * (N + 1) * (N + 1) + 2 * (N + 1) * (N + 1) + 2 * 4 * 33);
+    return sizeof(double) * ((size_t)32 * (N + 1) * (N + 1) + 2 * (N + 1) * (N + 1) + 2 * 4 * 34);
 }
 
 template <int N, int TRANS, int RED, bool JAC>
@@ -191,41 +195,45 @@ __global__ void __launch_bounds__(SegTune<N>::threads, SegTune<N>::minb) k_seg(
     RedAcc ra;
     const long long rowbase = (((long long)kl * g.ny + j) * g.nseg + seg) * rowlen;
     const double *Xrow = X + rowbase;
+    const bool has_prev = seg > 0, has_next = seg < g.nseg - 1;
     if (j < g.ny) {
-        // stage the own row (32*U doubles) in shared memory: 16-byte cp.async, L2 only
+        // everything the row needs from HBM goes through cp.async (L2 only),
+        // split over the warps of the row: the own row (32*U doubles), the
+        // four sigma_t / sigma_s rows of the staggered site sets, the x+1
+        // sample of lane 31, and the segment-edge values of the neighbours
 #pragma unroll 4
         for (int q = lane + 32 * half; q < 16 * U; q += 32 * WPR) cp_async16(xs + 2 * q, Xrow + 2 * q);
+        for (int q = lane + 32 * half; q < 128; q += 32 * WPR) {
+            const int rowq = q >> 4, part = (q & 15) * 2, fld = rowq >> 2, r4 = rowq & 3;
+            const int jj = min(j + (r4 & 1), g.ny - 1);
+            const int kk = kl + (r4 >> 1);   // plane nzl exists (edge-replicated at upload)
+            const long long vb = ((long long)kk * g.ny + jj) * g.nx + seg * 32;
+            cp_async16(sg + fld * 136 + r4 * 34 + part, (fld ? ss : st) + vb + part);
+        }
+        if (half == WPR - 1) {
+            if (lane < 8) {   // x+1 sample of lane 31 per sigma row, edge-replicated at nx-1
+                const int fld = lane >> 2, r4 = lane & 3;
+                const int jj = min(j + (r4 & 1), g.ny - 1);
+                const int kk = kl + (r4 >> 1);
+                const long long vb = ((long long)kk * g.ny + jj) * g.nx + seg * 32 + (has_next ? 32 : 31);
+                cp_async8(sg + fld * 136 + r4 * 34 + 32, (fld ? ss : st) + vb);
+            }
+            for (int c = lane; c < U; c += 32) {
+                if (has_prev) cp_async8(ep + c, Xrow - rowlen + c * 32 + 31);
+                else ep[c] = 0.0;
+                if (has_next) cp_async8(en + c, Xrow + rowlen + c * 32);
+                else en[c] = 0.0;
+            }
+        }
         cp_async_commit();
     }
-    // predicated on the solver's stop flag (CTA-uniform), read while the copy is in flight
+    // predicated on the solver's stop flag (CTA-uniform), read while the copies are in flight
     if (state && seg_stopped(state)) {
         cp_async_wait<0>();
         return;
     }
     if (j < g.ny) {
-        // x-edge values of the adjacent segments and the sigma rows, meanwhile
-        const bool has_prev = seg > 0, has_next = seg < g.nseg - 1;
-        if (half == WPR - 1) {
-            for (int c = lane; c < U; c += 32) {
-                ep[c] = has_prev ? __ldg(Xrow - rowlen + c * 32 + 31) : 0.0;
-                en[c] = has_next ? __ldg(Xrow + rowlen + c * 32) : 0.0;
-            }
-        }
         const int i = seg * 32 + lane;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            if (half != 0) break;
-            const int jj = min(j + (q & 1), g.ny - 1);
-            const int kk = kl + (q >> 1);   // plane nzl exists (edge-replicated at upload)
-            const long long vb = ((long long)kk * g.ny + jj) * g.nx + seg * 32;
-            sg[q * 33 + lane] = __ldg(st + vb + lane);
-            sg[132 + q * 33 + lane] = __ldg(ss + vb + lane);
-            if (lane == 0) {
-                const int off = has_next ? 32 : 31;   // x+1 of lane 31, edge-replicated at nx-1
-                sg[q * 33 + 32] = __ldg(st + vb + off);
-                sg[132 + q * 33 + 32] = __ldg(ss + vb + off);
-            }
-        }
         cp_async_wait<0>();
         if (WPR == 1) __syncwarp();
         else asm volatile("bar.sync %0, %1;\n" ::"r"(1 + rw), "r"(32 * WPR) : "memory");
