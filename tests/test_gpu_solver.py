@@ -248,3 +248,45 @@ def test_csr_faithful_bit_identical_to_reference(case, jac, golden):
     assert rep.iterations == meta[f"cg{jac}"]["iterations"]
     assert x.tobytes() == g[f"{case}/cg{jac}/x"].tobytes()
     assert np.array(rep.normal_history).tobytes() == g[f"{case}/cg{jac}/nh"].tobytes()
+
+
+# ---------------------------------------------------------------------------
+# C ABI error behaviour and native-path evidence
+# ---------------------------------------------------------------------------
+
+def test_abi_error_codes():
+    import ctypes
+    import scipy.sparse as sp
+    from paper_1807_00410_b200 import _lib
+    from paper_1807_00410_b200.solver import PnContext
+    L = _lib.load()
+    spec = rand_spec(1, (4, 4, 4), 1)
+    c = PnContext(build_tables(1), spec.res, spec.h)
+    with pytest.raises(ValueError):                        # bad field slot
+        _lib.check(L.pn_set_field(c.handle, 999, 0, 0.0, None, None))
+    with pytest.raises(ValueError):                        # setup not called
+        c.solve(tol=1e-6)
+    c.set_fields(spec)
+    with pytest.raises(ValueError):                        # tol <= 0 (solver.py:200-201)
+        c.solve(tol=0.0)
+    csr = PnContext.from_csr(sp.identity(5, format="csr"))
+    with pytest.raises(NotImplementedError):               # stencil-only entry point
+        csr.unstagger(np.zeros(5))
+    with pytest.raises(ValueError):                        # CSR solve needs b
+        csr.solve(tol=1e-6)
+    assert "tolerance" in L.pn_last_error().decode() or L.pn_last_error()
+
+
+def test_native_kernels_ran():
+    """The solve runs in libpnrte_b200.so: its kernel counter moves and the
+    library is mapped into this process."""
+    from paper_1807_00410_b200 import _lib
+    from paper_1807_00410_b200.solver import PnContext
+    spec = rand_spec(3, (32, 4, 4), 3)
+    c = PnContext(build_tables(3), spec.res, spec.h)
+    c.set_fields(spec)
+    n0 = c.kernel_launches()
+    c.solve(tol=1e-8, max_iter=50)
+    assert c.kernel_launches() > n0
+    maps = open("/proc/self/maps").read()
+    assert str(_lib.LIB_PATH) in maps
