@@ -154,10 +154,10 @@ int launch_csr_apply(pn_context *c, int trans, int faithful, int squared, const 
     const State *st = gated ? c->state : nullptr;
     const long long stride = (long long)c->g.nz * c->red_bx;
     if (faithful)
-        k_csr_apply<true><<<c->red_bx, 256, 0, s>>>(o.n, p, j, a, squared, x, y, red, minv, zt, c->partials, stride,
+        k_csr_apply<true><<<c->vec_bx, 256, 0, s>>>(o.n, p, j, a, squared, x, y, red, minv, zt, c->partials, stride,
                                                     c->red_bx, st);
     else
-        k_csr_apply<false><<<c->red_bx, 256, 0, s>>>(o.n, p, j, a, squared, x, y, red, minv, zt, c->partials, stride,
+        k_csr_apply<false><<<c->vec_bx, 256, 0, s>>>(o.n, p, j, a, squared, x, y, red, minv, zt, c->partials, stride,
                                                      c->red_bx, st);
     PN_CUDA(cudaGetLastError());
     c->launches++;

@@ -118,7 +118,8 @@ struct pn_context {
     bool bench_ready = false;
 
     // reductions
-    int red_bx = 0;               // blocks per plane for reductions
+    int red_bx = 0;               // partial slots per plane (stride of the partials array)
+    int vec_bx = 0;               // blocks per plane of the vector / table / dot kernels
     double *partials = nullptr;   // [RED_SLOTS][nz][red_bx] block partials (global plane index)
     double *plane_sums = nullptr; // [RED_SLOTS][nz] level-1 sums (all-gathered across ranks)
     double *ddot_chunks = nullptr;// faithful ddot chunk results [4][64]
@@ -171,7 +172,7 @@ int launch_apply_faithful(pn_context *c, int trans, int squared, const double *x
 int launch_xr(pn_context *c, cudaStream_t s);
 int launch_r_update(pn_context *c, cudaStream_t s);
 int launch_xp_update(pn_context *c, const double *zt, cudaStream_t s);
-int launch_plane_sums(pn_context *c, int mask, cudaStream_t s);
+int launch_plane_sums(pn_context *c, int mask, int cnt, cudaStream_t s);
 int launch_pupd(pn_context *c, const double *zt, cudaStream_t s);
 int launch_dot(pn_context *c, const double *a, const double *b, int slot, cudaStream_t s, bool gated = false);
 int launch_ddot_emul(pn_context *c, const double *a, const double *b, long long n, int slot, int threads,

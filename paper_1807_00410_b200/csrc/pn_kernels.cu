@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(256) k_apply_table(Tables T, Fields F, Geo g, 
                                                      const double *__restrict__ x, double *__restrict__ y,
                                                      const double *__restrict__ diag, int red, const double *minv,
                                                      double *zt, double *partials, long long slot_stride, int rb,
-                                                     const State *st, int kl0, int kst) {
+                                                     const State *st, int kl0, int kst, int pst) {
     if (st && stopped(st)) return;
     extern __shared__ unsigned char smem_raw[];
     const int U = g.U;
@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(256) k_apply_table(Tables T, Fields F, Geo g, 
         }
     }
     if (red) {
-        const long long idx = (long long)kg * rb + blockIdx.x;
+        const long long idx = (long long)kg * pst + blockIdx.x;
         if (red == 1) {
             double v[1] = {acc_r[0]};
             const int sl[1] = {0};
@@ -276,20 +276,20 @@ int launch_apply_table(pn_context *c, int trans, int faithful, int squared, cons
                        const double *minv, double *zt, cudaStream_t s, bool gated, int kl0, int npl, int kst) {
     if (npl < 0) npl = c->g.nzl;
     if (npl <= 0) return PN_OK;
-    dim3 grid(c->red_bx, npl);
+    dim3 grid(c->vec_bx, npl);
     size_t sm = table_smem(c, trans);
     const State *st = gated ? c->state : nullptr;
     bool recompute = !faithful && c->canonical_diag && c->uniform_phase;
     if (!recompute && !c->diag_ready) { set_error("internal: diagonal not assembled"); return PN_ERR_INVALID; }
     if (faithful) {
         k_apply_table<true, false><<<grid, 256, sm, s>>>(c->tb, c->f, c->g, trans, squared, x, y, c->diag, red, minv,
-                                                         zt, c->partials, slot_stride(c), c->red_bx, st, kl0, kst);
+                                                         zt, c->partials, slot_stride(c), c->vec_bx, st, kl0, kst, c->red_bx);
     } else if (recompute) {
         k_apply_table<false, true><<<grid, 256, sm, s>>>(c->tb, c->f, c->g, trans, 0, x, y, c->diag, red, minv, zt,
-                                                         c->partials, slot_stride(c), c->red_bx, st, kl0, kst);
+                                                         c->partials, slot_stride(c), c->vec_bx, st, kl0, kst, c->red_bx);
     } else {
         k_apply_table<false, false><<<grid, 256, sm, s>>>(c->tb, c->f, c->g, trans, 0, x, y, c->diag, red, minv, zt,
-                                                          c->partials, slot_stride(c), c->red_bx, st, kl0, kst);
+                                                          c->partials, slot_stride(c), c->vec_bx, st, kl0, kst, c->red_bx);
     }
     PN_CUDA(cudaGetLastError());
     c->launches++;
@@ -330,7 +330,7 @@ __global__ void __launch_bounds__(256) k_vec(int op, Geo g, double *y, const dou
 // fast fused x/r update with ||r||^2 partials (slot 3)
 __global__ void __launch_bounds__(256) k_xr(Geo g, double *__restrict__ x, double *__restrict__ r,
                                             const double *__restrict__ p, const double *__restrict__ w, const State *st,
-                                            double *partials, long long slot_stride, int rb) {
+                                            double *partials, long long slot_stride, int rb, int pst) {
     if (stopped(st)) return;
     const int kl = blockIdx.y;
     const long long chunk = (g.plane + rb - 1) / rb;
@@ -348,13 +348,13 @@ __global__ void __launch_bounds__(256) k_xr(Geo g, double *__restrict__ x, doubl
     }
     double v[1] = {acc};
     const int sl[1] = {3};
-    block_partials<1>(v, partials, sl, slot_stride, (long long)(g.z0 + kl) * rb + blockIdx.x);
+    block_partials<1>(v, partials, sl, slot_stride, (long long)(g.z0 + kl) * pst + blockIdx.x);
 }
 
 // fast r -= alpha w with ||r||^2 partials (slot 3); x is updated later,
 // fused with the p update (k_xp), with the same alpha and p (bitwise equal)
 __global__ void __launch_bounds__(256) k_r(Geo g, double *__restrict__ r, const double *__restrict__ w,
-                                           const State *st, double *partials, long long slot_stride, int rb) {
+                                           const State *st, double *partials, long long slot_stride, int rb, int pst) {
     if (stopped(st)) return;
     const int kl = blockIdx.y;
     const long long chunk = (g.plane + rb - 1) / rb;
@@ -371,7 +371,7 @@ __global__ void __launch_bounds__(256) k_r(Geo g, double *__restrict__ r, const 
     }
     double v[1] = {acc};
     const int sl[1] = {3};
-    block_partials<1>(v, partials, sl, slot_stride, (long long)(g.z0 + kl) * rb + blockIdx.x);
+    block_partials<1>(v, partials, sl, slot_stride, (long long)(g.z0 + kl) * pst + blockIdx.x);
 }
 
 // fast x += alpha p_old ; p = zt + beta p_old (p only while not stopped).
@@ -414,7 +414,7 @@ __global__ void __launch_bounds__(256) k_pupd(Geo g, double *__restrict__ p, con
 // deterministic dot products into slot (per plane-block partials)
 __global__ void __launch_bounds__(256) k_dot(Geo g, const double *__restrict__ a, const double *__restrict__ b,
                                              int slot, double *partials, long long slot_stride, int rb,
-                                             const State *st) {
+                                             const State *st, int pst) {
     if (st && stopped(st)) return;
     const int kl = blockIdx.y;
     const long long chunk = (g.plane + rb - 1) / rb;
@@ -425,53 +425,54 @@ __global__ void __launch_bounds__(256) k_dot(Geo g, const double *__restrict__ a
     for (long long rp = r0 + threadIdx.x; rp < r1; rp += blockDim.x) acc = fma(a[base + rp], b[base + rp], acc);
     double v[1] = {acc};
     const int sl[1] = {slot};
-    block_partials<1>(v, partials, sl, slot_stride, (long long)(g.z0 + kl) * rb + blockIdx.x);
+    block_partials<1>(v, partials, sl, slot_stride, (long long)(g.z0 + kl) * pst + blockIdx.x);
 }
 
 int launch_vec(pn_context *c, int op, double *y, const double *a, const double *b, cudaStream_t s, bool gated) {
-    dim3 grid(c->red_bx, c->g.nzl);
-    k_vec<<<grid, 256, 0, s>>>(op, c->g, y, a, b, c->state, c->partials, slot_stride(c), c->red_bx, gated ? 1 : 0);
+    dim3 grid(c->vec_bx, c->g.nzl);
+    k_vec<<<grid, 256, 0, s>>>(op, c->g, y, a, b, c->state, c->partials, slot_stride(c), c->vec_bx, gated ? 1 : 0);
     PN_CUDA(cudaGetLastError());
     c->launches++;
     return PN_OK;
 }
 
 int launch_xr(pn_context *c, cudaStream_t s) {
-    dim3 grid(c->red_bx, c->g.nzl);
+    dim3 grid(c->vec_bx, c->g.nzl);
     k_xr<<<grid, 256, 0, s>>>(c->g, c->x.p, c->r.p, c->p.p, c->w.p, c->state, c->partials, slot_stride(c),
-                              c->red_bx);
+                              c->vec_bx, c->red_bx);
     PN_CUDA(cudaGetLastError());
     c->launches++;
     return PN_OK;
 }
 
 int launch_r_update(pn_context *c, cudaStream_t s) {
-    dim3 grid(c->red_bx, c->g.nzl);
-    k_r<<<grid, 256, 0, s>>>(c->g, c->r.p, c->w.p, c->state, c->partials, slot_stride(c), c->red_bx);
+    dim3 grid(c->vec_bx, c->g.nzl);
+    k_r<<<grid, 256, 0, s>>>(c->g, c->r.p, c->w.p, c->state, c->partials, slot_stride(c), c->vec_bx, c->red_bx);
     PN_CUDA(cudaGetLastError());
     c->launches++;
     return PN_OK;
 }
 
 int launch_xp_update(pn_context *c, const double *zt, cudaStream_t s) {
-    dim3 grid(c->red_bx, c->g.nzl);
-    k_xp<<<grid, 256, 0, s>>>(c->g, c->x.p, c->p.p, zt, c->state, c->red_bx);
+    dim3 grid(c->vec_bx, c->g.nzl);
+    k_xp<<<grid, 256, 0, s>>>(c->g, c->x.p, c->p.p, zt, c->state, c->vec_bx);
     PN_CUDA(cudaGetLastError());
     c->launches++;
     return PN_OK;
 }
 
 int launch_pupd(pn_context *c, const double *zt, cudaStream_t s) {
-    dim3 grid(c->red_bx, c->g.nzl);
-    k_pupd<<<grid, 256, 0, s>>>(c->g, c->p.p, zt, c->state, c->red_bx);
+    dim3 grid(c->vec_bx, c->g.nzl);
+    k_pupd<<<grid, 256, 0, s>>>(c->g, c->p.p, zt, c->state, c->vec_bx);
     PN_CUDA(cudaGetLastError());
     c->launches++;
     return PN_OK;
 }
 
 int launch_dot(pn_context *c, const double *a, const double *b, int slot, cudaStream_t s, bool gated) {
-    dim3 grid(c->red_bx, c->g.nzl);
-    k_dot<<<grid, 256, 0, s>>>(c->g, a, b, slot, c->partials, slot_stride(c), c->red_bx, gated ? c->state : nullptr);
+    dim3 grid(c->vec_bx, c->g.nzl);
+    k_dot<<<grid, 256, 0, s>>>(c->g, a, b, slot, c->partials, slot_stride(c), c->vec_bx, gated ? c->state : nullptr,
+                               c->red_bx);
     PN_CUDA(cudaGetLastError());
     c->launches++;
     return PN_OK;
@@ -563,14 +564,14 @@ int launch_ddot_emul(pn_context *c, const double *a, const double *b, long long 
 // the nz plane values (level 2); multi-GPU ranks all-gather plane sums, so
 // the result does not depend on the slab decomposition.
 __global__ void __launch_bounds__(256) k_plane_sums(const double *__restrict__ partials, double *__restrict__ plane_sums,
-                                                    long long slot_stride, int rb, int nz, int z0, int mask) {
+                                                    long long slot_stride, int rb, int nz, int z0, int mask, int cnt) {
     const int slot = blockIdx.y;
     if (!(mask >> slot & 1)) return;
     const int kg = z0 + blockIdx.x;
     const double *p = partials + slot * slot_stride + (long long)kg * rb;
     __shared__ double sh[256];
     double acc = 0.0;
-    for (int i = threadIdx.x; i < rb; i += blockDim.x) acc = __dadd_rn(acc, p[i]);
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) acc = __dadd_rn(acc, p[i]);
     sh[threadIdx.x] = acc;
     __syncthreads();
     for (int o = 128; o > 0; o >>= 1) {
@@ -580,9 +581,10 @@ __global__ void __launch_bounds__(256) k_plane_sums(const double *__restrict__ p
     if (threadIdx.x == 0) plane_sums[slot * nz + kg] = sh[0];
 }
 
-int launch_plane_sums(pn_context *c, int mask, cudaStream_t s) {
+int launch_plane_sums(pn_context *c, int mask, int cnt, cudaStream_t s) {
     dim3 grid(c->g.nzl, RED_SLOTS);
-    k_plane_sums<<<grid, 256, 0, s>>>(c->partials, c->plane_sums, slot_stride(c), c->red_bx, c->g.nz, c->g.z0, mask);
+    k_plane_sums<<<grid, 256, 0, s>>>(c->partials, c->plane_sums, slot_stride(c), c->red_bx, c->g.nz, c->g.z0, mask,
+                                      cnt);
     PN_CUDA(cudaGetLastError());
     c->launches++;
     return PN_OK;

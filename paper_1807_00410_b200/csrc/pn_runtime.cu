@@ -28,6 +28,7 @@
 
 #include "pn_internal.cuh"
 #include "pn_seg.cuh"
+#include "pn_seg_types.cuh"
 
 namespace pn {
 
@@ -113,8 +114,8 @@ static int halo_exchange(std::vector<pn_context *> &cs, Buf pn_context::*vec, cu
 
 // slots: bit mask of reduction slots every rank needs.  Block partials are
 // folded into per-plane sums locally; the plane sums are all-gathered.
-static int gather_partials(std::vector<pn_context *> &cs, int slots, cudaStream_t s) {
-    for (auto *c : cs) PN_TRY(launch_plane_sums(c, slots, s));
+static int gather_partials(std::vector<pn_context *> &cs, int slots, cudaStream_t s, int nparts = -1) {
+    for (auto *c : cs) PN_TRY(launch_plane_sums(c, slots, nparts < 0 ? c->vec_bx : nparts, s));
     pn_context *c0 = cs[0];
     if (c0->world <= 1) return PN_OK;
     const long long nz = c0->g.nz, cnt = c0->g.nzl;
@@ -140,7 +141,8 @@ static void pick_red_bx(pn_context *c) {
     long long target = 2LL * 148 * 8;
     long long bx = (target + c->g.nz - 1) / c->g.nz;
     long long maxb = (c->g.plane + 255) / 256;
-    c->red_bx = (int)std::max(1LL, std::min(bx, maxb));
+    c->vec_bx = (int)std::max(1LL, std::min(bx, maxb));
+    c->red_bx = c->vec_bx;
 }
 
 }  // namespace pn
@@ -210,7 +212,13 @@ int pn_create(const pn_desc *d, pn_context **out) {
     if (st != PN_OK) { pn_destroy(c); return st; }
     c->f.n = d->n_fields;
     pick_red_bx(c);
-    if (pn_seg_red_blocks(c) > 0) c->red_bx = pn_seg_red_blocks(c);
+    // the segmented kernel writes one partial per warp; the vector kernels keep
+    // their own (smaller) blocking inside the same per-plane stride
+    if (pn_seg_red_blocks(c) > 0) {
+        const int warps = seg_rows(c->N) * (seg_pair(c->N) ? 2 : 1);
+        c->vec_bx = std::max(1, pn_seg_red_blocks(c) / warps);   // segments x row blocks per plane
+        c->red_bx = pn_seg_red_blocks(c);
+    }
     st = dalloc(c, &c->partials, (size_t)RED_SLOTS * g.nz * c->red_bx);
     if (st == PN_OK) st = dalloc(c, &c->plane_sums, (size_t)RED_SLOTS * g.nz);
     if (st == PN_OK) st = dalloc(c, &c->ddot_chunks, 4 * 64);
@@ -261,6 +269,7 @@ int pn_create_csr(int64_t n, int64_t nnz, const int64_t *indptr, const int32_t *
     int st = csr_build(c, n, nnz, (const long long *)indptr, indices, data);
     if (st == PN_OK) {
         c->red_bx = (int)std::max<long long>(1, std::min<long long>((n + 255) / 256, 2 * 148 * 8));
+        c->vec_bx = c->red_bx;
         st = dalloc(c, &c->partials, (size_t)RED_SLOTS * c->red_bx);
     }
     if (st == PN_OK) st = dalloc(c, &c->plane_sums, RED_SLOTS);
@@ -432,8 +441,9 @@ static int group_apply(std::vector<pn_context *> &cs, int trans, int faithful, B
                                 nzl > 1 ? 2 : 1, nzl > 1 ? nzl - 1 : 1));
         }
     }
-    if (red == 1) PN_TRY(gather_partials(cs, 1, s));
-    if (red == 2) PN_TRY(gather_partials(cs, 2 | 4, s));
+    const int cnt = (seg && !faithful) ? pn_seg_red_blocks(c0) : c0->vec_bx;
+    if (red == 1) PN_TRY(gather_partials(cs, 1, s, cnt));
+    if (red == 2) PN_TRY(gather_partials(cs, 2 | 4, s, cnt));
     return PN_OK;
 }
 

@@ -25,7 +25,9 @@ static bool seg_geometry_ok(const pn_context *c) {
 
 int pn_seg_red_blocks(const pn_context *c) {
     if (!seg_geometry_ok(c)) return 0;
-    return (c->g.nx / 32) * ((c->g.ny + seg_rows(c->N) - 1) / seg_rows(c->N));
+    // one reduction partial per warp: segments x row blocks x warps per CTA
+    const int warps = seg_rows(c->N) * (seg_pair(c->N) ? 2 : 1);
+    return (c->g.nx / 32) * ((c->g.ny + seg_rows(c->N) - 1) / seg_rows(c->N)) * warps;
 }
 
 bool pn_seg_ok(const pn_context *c) { return c->seg && ((SegCtx *)c->seg)->ok; }
@@ -37,7 +39,7 @@ int pn_seg_prepare(pn_context *c, cudaStream_t) {
         c->seg = sc;
     }
     sc->ok = false;
-    if (!seg_geometry_ok(c) || !c->uniform_phase || c->red_bx != pn_seg_red_blocks(c)) return PN_OK;
+    if (!seg_geometry_ok(c) || !c->uniform_phase || c->red_bx < pn_seg_red_blocks(c)) return PN_OK;
     if (c->f.kind[0] != 2 || c->f.kind[1] != 2) return PN_OK;   // sigma arrays (uniform ones are materialised)
     if (!sc->pa) {
         sc->pa = new SegParams();

@@ -273,7 +273,8 @@ __global__ void __launch_bounds__(SegTune<N>::threads, SegTune<N>::minb) k_seg(
         }
     }
     if (RED) {
-        __shared__ double red[3][SegTune<N>::rows * SegTune<N>::wpr];
+        // one partial per warp (fixed slot, no CTA barrier): warp tree, lane 0 stores
+        constexpr int W = SegTune<N>::rows * SegTune<N>::wpr;
         double v0 = ra.s0, v1 = ra.s1, v2 = (RED == 2 && !JAC) ? ra.s1 : ra.s2;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
@@ -281,15 +282,10 @@ __global__ void __launch_bounds__(SegTune<N>::threads, SegTune<N>::minb) k_seg(
             v1 += __shfl_down_sync(0xffffffffu, v1, o);
             v2 += __shfl_down_sync(0xffffffffu, v2, o);
         }
-        if (lane == 0) { red[0][warp] = v0; red[1][warp] = v1; red[2][warp] = v2; }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-#pragma unroll
-            for (int w = 0; w < SegTune<N>::rows * SegTune<N>::wpr; ++w) { a0 += red[0][w]; a1 += red[1][w]; a2 += red[2][w]; }
-            const long long idx = (long long)kg * rb + (long long)seg * g.nyb + jb;
-            if (RED == 1) partials[idx] = a0;
-            if (RED == 2) { partials[1 * slot_stride + idx] = a1; partials[2 * slot_stride + idx] = a2; }
+        if (lane == 0 && jb < g.nyb) {
+            const long long idx = (long long)kg * rb + ((long long)seg * g.nyb + jb) * W + warp;
+            if (RED == 1) partials[idx] = v0;
+            if (RED == 2) { partials[1 * slot_stride + idx] = v1; partials[2 * slot_stride + idx] = v2; }
         }
     }
 }
