@@ -102,7 +102,8 @@ class StencilOracle:
         from paper_1807_00410_b200.program import field_slots, pack_tables
         from paper_1807_00410_b200.problems import field_slot
         self.tables = tables
-        self.res = tuple(int(r) for r in spec.res)
+        self.shape = tuple(int(r) for r in spec.res)
+        self.res = self.shape + (1,) * (3 - len(self.shape))   # 2-D programs: nz = 1
         self.U = tables.U
         self.nvox = int(np.prod(self.res))
         self.R = self.nvox * self.U
@@ -112,7 +113,7 @@ class StencilOracle:
         for name, _ in _Tables._fields_[4:]:
             setattr(t, name, _ptr(self.pk[name]))
         self._t = t
-        names = field_slots(tables.N)
+        names = field_slots(tables)
         self._kind = np.zeros(len(names), np.int32)
         self._scalar = np.zeros(len(names), np.float64)
         self._arrays = []
@@ -121,7 +122,7 @@ class StencilOracle:
             kind, scal, arr = field_slot(spec, name)
             self._kind[s], self._scalar[s] = kind, scal
             if kind == 2:
-                a = np.ascontiguousarray(np.asarray(arr, np.float64).transpose(2, 1, 0))
+                a = np.ascontiguousarray(np.asarray(arr, np.float64).reshape(self.res).transpose(2, 1, 0))
                 self._arrays.append(a)
                 ptrs[s] = a.ctypes.data
         self._ptrs = ptrs
@@ -173,7 +174,7 @@ class StencilOracle:
         u = np.ascontiguousarray(u, np.float64)
         out = np.empty(self.res + (self.U,))
         lib().or_unstagger(ctypes.byref(self._t), _ptr(u), _ptr(out))
-        return out
+        return out.reshape(self.shape + (self.U,))
 
 
 def _cgnr(op, n, b, tol, max_iter, primal_tol, jacobi, x0, th, kn, jac_fn):

@@ -162,7 +162,7 @@ int pn_nccl_unique_id(void *out128) {
 
 int pn_create(const pn_desc *d, pn_context **out) {
     if (!d || !out) { set_error("null argument"); return PN_ERR_INVALID; }
-    if (d->U != (d->N + 1) * (d->N + 1) || d->nx < 1 || d->ny < 1 || d->nz < 1 || d->nz_local < 1 || d->z0 < 0 ||
+    if (d->U < 1 || d->U > 64 || d->nx < 1 || d->ny < 1 || d->nz < 1 || d->nz_local < 1 || d->z0 < 0 ||
         d->z0 + d->nz_local > d->nz) {
         set_error("invalid grid / slab");
         return PN_ERR_INVALID;

@@ -64,6 +64,24 @@ class ProblemSpec:
         return self.origin[axis] + (np.arange(self.res[axis]) + 0.5) * self.h
 
 
+def make_checkerboard(res=71):
+    """2-D lattice problem (problems.py:104-127): 7x7 domain, absorbing
+    checkerboard on the inner 5x5 blocks, unit isotropic emitter in the centre
+    block.  Restated so 2-D fixtures can be rebuilt without the reference."""
+    n = res
+    xs = (np.arange(n) + 0.5) * (7.0 / n)
+    bx = np.floor(xs).astype(int)
+    BX, BY = np.meshgrid(bx, bx, indexing="ij")
+    absorber = ((BX + BY) % 2 == 0) & (BX >= 1) & (BX <= 5) & (BY >= 1) & (BY <= 5) & ~((BX == 3) & (BY == 3))
+    sigma_t = np.where(absorber, 10.0, 1.0)
+    sigma_s = np.where(absorber, 0.0, 1.0)
+    q00 = np.where((BX == 3) & (BY == 3), 1.0 / math.sqrt(4.0 * math.pi), 0.0)
+    fields = {"sigma_t": sigma_t, "sigma_s": sigma_s, "Q_0_0": q00}
+    fields.update(phase_fields(0.0, 8))
+    return ProblemSpec(dim=2, origin=(0.0, 0.0), extent=(7.0, 7.0), res=(n, n), fields=fields,
+                       bc="dirichlet", sigma_t_floor=1.0, name="checkerboard")
+
+
 def validate_for_solve(spec):
     """Admission: any sigma_t <= 0 makes the system singular."""
     st = np.asarray(spec.field_array("sigma_t"))

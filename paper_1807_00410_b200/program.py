@@ -92,6 +92,7 @@ class PnTables:
     N: int
     U: int
     rows: tuple          # indexed by component
+    dim: int = 3         # 2-D programs are embedded as nz = 1 grids (z parity / offsets 0)
 
     @property
     def lm(self):
@@ -345,7 +346,13 @@ def _kind(node):
 
 
 def _site(pos):
-    return tuple(p // 2 for p in pos)
+    s = tuple(p // 2 for p in pos)
+    return s + (0,) * (AXES - len(s))
+
+
+def _pad3(t):
+    t = tuple(t)
+    return t + (0,) * (AXES - len(t))
 
 
 def _term(node):
@@ -394,29 +401,28 @@ def _hinv_weights(expr):
 
 def tables_from_program(program):
     """Flatten a reference StencilProgram (stencil.py:205-217) into tables."""
-    if program.dim != 3:
-        raise UnsupportedProgramError("the matrix-free path is 3-D only")
+    if program.dim not in (2, 3):
+        raise UnsupportedProgramError("programs must be 2-D or 3-D")
     U = len(program.rows)
-    if U != (program.N + 1) ** 2:
-        raise UnsupportedProgramError("not a full 3-D P_N program")
-    place = program.placement.offsets
+    place = {k: _pad3(v) for k, v in program.placement.offsets.items()}
     rows = []
     for row in program.rows:
         comp = program.unknown_index[row.index]
-        loc = tuple(row.location)
+        loc = _pad3(row.location)
         entries = []
         for e in row.entries:
             home = place[e.target]
-            disp = tuple((e.offset[k] - home[k]) // 2 for k in range(AXES))
+            off = _pad3(e.offset)
+            disp = tuple((off[k] - home[k]) // 2 for k in range(AXES))
             tc = program.unknown_index[e.target]
             is_diag = tc == comp and disp == (0, 0, 0)
             if is_diag:
-                entries.append(Entry(tc, tuple(e.target), tuple(e.offset), disp,
+                entries.append(Entry(tc, tuple(e.target), off, disp,
                                      True, (), _terms(e.coeff)))
             else:
                 if sum(1 for d in disp if d != 0) > 1 or any(abs(d) > 1 for d in disp):
                     raise UnsupportedProgramError("stencil reach beyond one voxel")
-                entries.append(Entry(tc, tuple(e.target), tuple(e.offset), disp,
+                entries.append(Entry(tc, tuple(e.target), off, disp,
                                      False, _hinv_weights(e.coeff), ()))
         res = row.residual
         rhs = () if (_kind(res) == "Num" and float(res.value) == 0.0) else _terms(res)
@@ -424,7 +430,7 @@ def tables_from_program(program):
     rows.sort(key=lambda r: r.comp)
     if [r.comp for r in rows] != list(range(U)):
         raise UnsupportedProgramError("component indices are not 0..U-1")
-    return PnTables(N=program.N, U=U, rows=tuple(rows))
+    return PnTables(N=program.N, U=U, rows=tuple(rows), dim=program.dim)
 
 
 def as_tables(program_or_N):
@@ -445,6 +451,8 @@ def canonical_diag(tables):
     + sum_{s1,s2} (-lambda_l/n^2) sigma_s@s1 p_l@s2  over the staggered
     site set of its row: then diag = avg(sigma_t) - lambda_l p_l avg(sigma_s)
     for spatially uniform p_l, which the fast kernels recompute on the fly."""
+    if tables.dim != 3 or tables.U != (tables.N + 1) ** 2:
+        return False
     ref = build_tables(tables.N)
     for a, b in zip(ref.rows, tables.rows):
         da = [e for e in a.entries if e.diag][0]
@@ -454,11 +462,25 @@ def canonical_diag(tables):
     return True
 
 
+def from_json(d):
+    """Inverse of to_json (tables of 2-D programs come from fixtures)."""
+    def term(t):
+        return Term(t[0], tuple((f, tuple(site)) for f, site in t[1]))
+    rows = []
+    for r in d["rows"]:
+        ents = tuple(Entry(e["target"], tuple(e["lm"]), tuple(e["offset"]), tuple(e["disp"]), e["diag"],
+                           tuple(e["weights"]), tuple(term(t) for t in e["terms"])) for e in r["entries"])
+        rows.append(Row(r["comp"], tuple(r["lm"]), tuple(r["location"]), ents, tuple(term(t) for t in r["rhs"])))
+    return PnTables(N=d["N"], U=d["U"], rows=tuple(rows), dim=d.get("dim", 3))
+
+
 def to_json(tables):
     """Stable JSON-able dump (golden fixture format)."""
     def term(t):
         return [t.coef, [[f, list(s)] for f, s in t.factors]]
     out = {"N": tables.N, "U": tables.U, "rows": []}
+    if tables.dim != 3:
+        out["dim"] = tables.dim
     for r in tables.rows:
         out["rows"].append({
             "comp": r.comp, "lm": list(r.lm), "location": list(r.location),
@@ -485,8 +507,14 @@ DIR_RANK = {5: 0, 3: 1, 1: 2, 0: 3, 2: 4, 4: 5, 6: 6}
 NEG_DIR = {0: 0, 1: 2, 2: 1, 3: 4, 4: 3, 5: 6, 6: 5}
 
 
-def field_slots(N):
-    """Device field slot order: sigma_t, sigma_s, p_0..p_N, Q_lm by comp."""
+def field_slots(N_or_tables):
+    """Device field slot order: sigma_t, sigma_s, p_0..p_N, Q_lm by comp
+    (for a 3-D order N, or for the rows of given tables, e.g. 2-D)."""
+    if isinstance(N_or_tables, PnTables):
+        t = N_or_tables
+        names = ["sigma_t", "sigma_s"] + [p_name(l) for l in range(t.N + 1)]
+        return names + [q_name(*r.lm) for r in t.rows]
+    N = N_or_tables
     names = ["sigma_t", "sigma_s"] + [p_name(l) for l in range(N + 1)]
     names += [q_name(l, m) for (l, m) in sorted(scope(N), key=lambda lm: comp_index(*lm))]
     return names
@@ -515,7 +543,7 @@ def pack_tables(tables, h):
     """Flatten tables (+ grid spacing h) into int32/float64 numpy arrays."""
     import numpy as np
     U = tables.U
-    slots = {n: i for i, n in enumerate(field_slots(tables.N))}
+    slots = {n: i for i, n in enumerate(field_slots(tables))}
     par = np.array([parity_bits(r.location) for r in tables.rows], np.int32)
     lam = np.array([lambda_l(r.lm[0]) for r in tables.rows], np.float64)
     lidx = np.array([r.lm[0] for r in tables.rows], np.int32)

@@ -90,7 +90,8 @@ class PnContext:
         torch = _torch()
         L = _lib.load()
         self.tables = tables
-        self.res = tuple(int(r) for r in res)
+        self.dim = len(tuple(res))
+        self.res = tuple(int(r) for r in res) + (1,) * (3 - len(tuple(res)))   # 2-D: nz = 1
         self.h = float(h)
         self.U = tables.U
         self.N = tables.N
@@ -146,6 +147,7 @@ class PnContext:
         data = np.ascontiguousarray(A.data, dtype=np.float64)
         self = cls.__new__(cls)
         self.tables = None
+        self.dim = 1
         self.N, self.U = 0, 1
         self.res = (A.shape[0], 1, 1)
         self.h = 1.0
@@ -181,11 +183,12 @@ class PnContext:
         held = []
         with torch.cuda.device(self.device):
             s = _stream(torch)
-            for slot, name in enumerate(field_slots(self.N)):
+            for slot, name in enumerate(field_slots(self.tables)):
                 kind, scal, arr = field_slot(spec, name)
                 ptr = None
                 if kind == 2:
-                    t = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float64)).to(self.dev, non_blocking=False)
+                    arr = np.asarray(arr, dtype=np.float64).reshape(self.res)   # 2-D fields: [i, j] -> [i, j, 1]
+                    t = torch.from_numpy(np.ascontiguousarray(arr)).to(self.dev, non_blocking=False)
                     held.append(t)
                     ptr = ctypes.c_void_p(t.data_ptr())
                 _lib.check(self._L.pn_set_field(self.handle, slot, kind, scal, ptr, s))
@@ -263,7 +266,7 @@ class PnContext:
         with torch.cuda.device(self.device):
             _lib.check(self._L.pn_unstagger(self.handle, ctypes.c_void_p(ut.data_ptr()),
                                             ctypes.c_void_p(out.data_ptr()), _stream(torch)))
-        return out
+        return out[:, :, 0] if getattr(self, "dim", 3) == 2 else out
 
     def bench(self, what, reps):
         ms = ctypes.c_double()
@@ -339,6 +342,8 @@ def _csr_from_tables(pk, res, diag):
 
 def _check_dim(program, spec):
     dim = getattr(program, "dim", 3)
+    if len(tuple(spec.res)) not in (2, 3):
+        raise ValueError("only 2-D and 3-D problems are supported")
     if len(tuple(spec.res)) != dim:
         raise ValueError(f"problem is {len(tuple(spec.res))}-D but program is {dim}-D")
 
@@ -393,8 +398,8 @@ def solve_pn(program_or_N, spec, tol=1e-8, max_iter=50000, primal_tol=None, jaco
              mode="fast", device=0, return_staggered=False, **kw):
     """The north-star entry point: order + fields in, (N+1)^2 collocated SH
     coefficients per voxel out (cli.py:136-155 without file I/O)."""
-    _check_dim(program_or_N if not isinstance(program_or_N, int) else None or type("p", (), {"dim": 3}), spec)
     tables = as_tables(program_or_N)
+    _check_dim(tables, spec)
     ctx = PnContext(tables, spec.res, spec.h, device=device)
     ctx.set_fields(spec)
     if tol <= 0:

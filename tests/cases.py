@@ -29,6 +29,23 @@ CASES = [
 ]
 
 
+# 2-D programs (checkerboard, problems.py:104-127): (name, N, res); tables
+# come from tests/golden/tables_N{N}_2d.json, the spec from make_checkerboard
+CASES_2D = [
+    ("cb_p1_15", 1, 15),
+    ("cb_p2_15", 2, 15),
+    ("cb_p3_21", 3, 21),
+]
+
+
+def tables_2d(N):
+    import json
+    import pathlib
+    from paper_1807_00410_b200.program import from_json
+    g = pathlib.Path(__file__).resolve().parent / "golden" / f"tables_N{N}_2d.json"
+    return from_json(json.loads(g.read_text()))
+
+
 def rand_spec(N, res, seed, g=0.6, q_frac=0.5, uniform_sigma=False):
     """Heterogeneous sigma_t in [0.5, 20), albedo in [0, 0.99), HG phase g,
     random emission on about q_frac of the (l, m) coefficients."""
@@ -51,3 +68,19 @@ def rand_spec(N, res, seed, g=0.6, q_frac=0.5, uniform_sigma=False):
 
 def probe_vector(R, seed=99):
     return np.random.default_rng(seed).normal(size=R)
+
+
+ALL_CASES = [c[0] for c in CASES] + [c[0] for c in CASES_2D]
+
+
+def case_inputs(name):
+    """(tables, spec) of a named fixture case, 3-D random or 2-D checkerboard."""
+    from paper_1807_00410_b200.problems import make_checkerboard
+    from paper_1807_00410_b200.program import build_tables
+    for cname, N, res, seed in CASES:
+        if cname == name:
+            return build_tables(N), rand_spec(N, res, seed)
+    for cname, N, n in CASES_2D:
+        if cname == name:
+            return tables_2d(N), make_checkerboard(n)
+    raise KeyError(name)

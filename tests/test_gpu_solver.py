@@ -290,3 +290,41 @@ def test_native_kernels_ran():
     assert c.kernel_launches() > n0
     maps = open("/proc/self/maps").read()
     assert str(_lib.LIB_PATH) in maps
+
+
+# ---------------------------------------------------------------------------
+# 2-D programs (reference test_solver.py:82-92, 148-155 use the checkerboard)
+# ---------------------------------------------------------------------------
+
+def test_2d_matvec_adjoint_consistency():
+    from cases import tables_2d
+    from paper_1807_00410_b200.problems import make_checkerboard
+    from paper_1807_00410_b200.solver import assemble
+    s = assemble(tables_2d(2), make_checkerboard(15))
+    assert s.A.shape[0] == 15 * 15 * 6
+    rng = np.random.default_rng(0)
+    for _ in range(5):
+        u, v = rng.normal(size=s.A.shape[0]), rng.normal(size=s.A.shape[0])
+        lhs, rhs = float((s.A @ u) @ v), float(u @ (s.A.T @ v))
+        assert abs(lhs - rhs) <= 1e-12 * (1 + abs(lhs))
+
+
+def test_2d_cg_residual_histories_recorded():
+    from cases import tables_2d
+    from paper_1807_00410_b200.problems import make_checkerboard
+    from paper_1807_00410_b200.solver import assemble, solve_normal_cg, unstagger
+    s = assemble(tables_2d(1), make_checkerboard(15))
+    x, rep = solve_normal_cg(s, tol=1e-10, max_iter=5000)
+    assert rep.converged and rep.normal_history[-1] <= 1e-10
+    assert len(rep.primal_history) == len(rep.normal_history)
+    assert rep.primal_residual < 1e-8
+    coll = unstagger(x, tables_2d(1), (15, 15))
+    assert coll.shape == (15, 15, 3)
+
+
+def test_2d_checkerboard_71_size():
+    """test_solver.py:58-61: the full checkerboard P1 system has 71*71*3 rows."""
+    from cases import tables_2d
+    from paper_1807_00410_b200.problems import make_checkerboard
+    from paper_1807_00410_b200.solver import assemble
+    assert assemble(tables_2d(1), make_checkerboard()).A.shape[0] == 71 * 71 * 3

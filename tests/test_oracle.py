@@ -6,7 +6,7 @@ import hashlib
 import numpy as np
 import pytest
 
-from cases import CASES, probe_vector, rand_spec
+from cases import ALL_CASES, CASES, case_inputs, probe_vector, rand_spec
 from oracle.oracle import StencilOracle, ddot
 from paper_1807_00410_b200.configs import make_config
 from paper_1807_00410_b200.program import build_tables
@@ -20,10 +20,10 @@ def sha(a):
 
 @pytest.fixture(scope="module")
 def oracles():
-    return {name: StencilOracle(build_tables(N), rand_spec(N, res, seed)) for name, N, res, seed in CASES}
+    return {name: StencilOracle(*case_inputs(name)) for name in ALL_CASES}
 
 
-@pytest.mark.parametrize("case", [c[0] for c in CASES])
+@pytest.mark.parametrize("case", ALL_CASES)
 def test_oracle_assembly_matches_golden(case, oracles, golden):
     o, g = oracles[case], golden["cases"]
     A = o.csr()
@@ -34,7 +34,7 @@ def test_oracle_assembly_matches_golden(case, oracles, golden):
     assert o.jacobi_diag().tobytes() == g[f"{case}/jac"].tobytes()
 
 
-@pytest.mark.parametrize("case", [c[0] for c in CASES])
+@pytest.mark.parametrize("case", ALL_CASES)
 def test_oracle_apply_matches_golden(case, oracles, golden):
     o, g = oracles[case], golden["cases"]
     x = probe_vector(o.R)
@@ -42,7 +42,7 @@ def test_oracle_apply_matches_golden(case, oracles, golden):
     assert o.apply(x, transpose=True).tobytes() == g[f"{case}/Atx"].tobytes()
 
 
-@pytest.mark.parametrize("case", [c[0] for c in CASES])
+@pytest.mark.parametrize("case", ALL_CASES)
 def test_oracle_cgnr_matches_golden(case, oracles, golden):
     o, g, meta = oracles[case], golden["cases"], golden["cases_meta"]["cases"][case]
     for jac in (0, 1):

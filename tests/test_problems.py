@@ -55,3 +55,14 @@ def test_spec_validation_mirrors_reference():
         floor_sigma_t(s, 0.0)
     fl = floor_sigma_t(s, 3.0)
     assert np.all(fl.field_array("sigma_t") == 3.0) and fl.sigma_t_floor == 3.0
+
+
+@pytest.mark.reference
+@pytest.mark.parametrize("n", [15, 21, 71])
+def test_checkerboard_generator_bit_identical(n, ref):
+    from pnrte.problems import make_checkerboard as ref_cb
+    from paper_1807_00410_b200.problems import make_checkerboard
+    a, b = make_checkerboard(n), ref_cb(n)
+    assert a.res == b.res and a.extent == b.extent and a.dim == b.dim == 2
+    for k in b.fields:
+        assert np.asarray(a.fields[k]).tobytes() == np.asarray(b.fields[k]).tobytes(), k

@@ -77,3 +77,22 @@ def test_pack_orders_columns_ascending():
             keys = [(rank[int(pk[f"{prefix}_dir"][e])], int(pk[oth][e])) for e in range(ptr[c], ptr[c + 1])]
             assert keys == sorted(keys)
     assert len(field_slots(5)) == pk["n_fields"] == 2 + 6 + 36
+
+
+@pytest.mark.parametrize("N", [1, 2, 3])
+def test_2d_tables_roundtrip_golden(N, golden):
+    from paper_1807_00410_b200.program import from_json
+    want = json.loads((golden["dir"] / f"tables_N{N}_2d.json").read_text())
+    t = from_json(want)
+    assert t.dim == 2 and to_json(t) == want
+    pk = pack_tables(t, 0.1)
+    assert set(pk["par"].tolist()) <= {0, 1, 2, 3}     # no z staggering in 2-D
+
+
+@pytest.mark.reference
+@pytest.mark.parametrize("N", [1, 2, 3])
+def test_2d_tables_match_live_reference(N, ref, golden):
+    from pnrte.equations import build_pn
+    from pnrte.stencil import compile_program
+    t = tables_from_program(compile_program(build_pn(N, 2)))
+    assert to_json(t) == json.loads((golden["dir"] / f"tables_N{N}_2d.json").read_text())

@@ -30,7 +30,8 @@ from pnrte.solver import assemble, solve_normal_cg, unstagger  # noqa: E402
 from pnrte.stencil import compile_program  # noqa: E402
 from threadpoolctl import threadpool_info  # noqa: E402
 
-from cases import CASES, probe_vector, rand_spec  # noqa: E402
+from cases import CASES, CASES_2D, probe_vector, rand_spec  # noqa: E402
+from paper_1807_00410_b200.problems import make_checkerboard  # noqa: E402
 from paper_1807_00410_b200.configs import make_config  # noqa: E402
 from paper_1807_00410_b200.program import tables_from_program, to_json  # noqa: E402
 
@@ -54,11 +55,15 @@ def main():
     for N in range(1, 8):
         t = tables_from_program(compile_program(build_pn(N, 3)))
         (GOLD / f"tables_N{N}.json").write_text(json.dumps(to_json(t), separators=(",", ":")))
+    for N in (1, 2, 3):
+        t = tables_from_program(compile_program(build_pn(N, 2)))
+        (GOLD / f"tables_N{N}_2d.json").write_text(json.dumps(to_json(t), separators=(",", ":")))
     arrs = {}
     meta = {"blas": blas(), "cases": {}}
-    for name, N, res, seed in CASES:
-        prog = compile_program(build_pn(N, 3))
-        spec = rand_spec(N, res, seed)
+    todo = [(name, N, res, rand_spec(N, res, seed), 3) for name, N, res, seed in CASES]
+    todo += [(name, N, (n, n), make_checkerboard(n), 2) for name, N, n in CASES_2D]
+    for name, N, res, spec, dim in todo:
+        prog = compile_program(build_pn(N, dim))
         sysm = assemble(prog, spec)
         A = sysm.A
         x = probe_vector(A.shape[0])
