@@ -264,6 +264,24 @@ def run_ours(args):
                 "algorithmic_bytes_per_launch": bytes_apply,
                 "bytes_formula": "8*nvox*(2U+2): read u, write A u, read sigma_t and sigma_s"}
 
+    # ---- the other single-GPU configurations' apply throughput (rank 0, context)
+    others = None
+    if rank == 0 and not args.skip_others:
+        others = {}
+        for idx in (1, 2, 3):
+            co = make_config(idx)
+            ctx_o = PnContext(build_tables(co.N), co.spec.res, co.spec.h, device=local)
+            ctx_o.set_fields(co.spec)
+            ctx_o.bench(0, 5)
+            ms_o = ctx_o.bench(0, 50)
+            U_o = (co.N + 1) ** 2
+            nv_o = int(np.prod(co.spec.res))
+            gbs = 8 * nv_o * (2 * U_o + 2) / (ms_o / 1e3) / 1e9
+            others[f"cfg{idx}"] = {"apply_ms": ms_o, "gunk_s": nv_o * U_o / (ms_o / 1e3) / 1e9,
+                                   "achieved_gbs": gbs, "frac": gbs / peak,
+                                   "note": "L2-resident working set" if idx <= 2 else "HBM-bound"}
+            del ctx_o
+
     # ---- time-to-residual 1e-6 on config 2 (single GPU, rank 0)
     ttr = None
     if rank == 0 and not args.skip_ttr:
@@ -331,6 +349,7 @@ def run_ours(args):
                              "what": "one fused CGNR iteration: A p + ww, alpha, x/r update + rr, A^T r + zz/zzt, "
                                      "beta, p update"},
             "time_to_residual": ttr,
+            "other_configs_apply": others,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -350,6 +369,7 @@ def main():
     ap.add_argument("--skip-ttr", action="store_true")
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--skip-others", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         log("warm-up raised to 3 (contract minimum)")

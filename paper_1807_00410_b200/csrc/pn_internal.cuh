@@ -169,11 +169,9 @@ int launch_apply_table(pn_context *c, int trans, int faithful, int squared, cons
                        int kst = 1);
 int launch_apply_faithful(pn_context *c, int trans, int squared, const double *x, double *y,
                           cudaStream_t s, bool gated = false);
-int launch_xr(pn_context *c, cudaStream_t s);
 int launch_r_update(pn_context *c, cudaStream_t s);
 int launch_xp_update(pn_context *c, const double *zt, cudaStream_t s);
 int launch_plane_sums(pn_context *c, int mask, int cnt, cudaStream_t s);
-int launch_pupd(pn_context *c, const double *zt, cudaStream_t s);
 int launch_dot(pn_context *c, const double *a, const double *b, int slot, cudaStream_t s, bool gated = false);
 int launch_ddot_emul(pn_context *c, const double *a, const double *b, long long n, int slot, int threads,
                      int kernel, cudaStream_t s, bool gated = false);

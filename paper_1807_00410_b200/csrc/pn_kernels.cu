@@ -126,12 +126,6 @@ __constant__ int c_dx[7] = {0, -1, 1, 0, 0, 0, 0};
 __constant__ int c_dy[7] = {0, 0, 0, -1, 1, 0, 0};
 __constant__ int c_dz[7] = {0, 0, 0, 0, 0, -1, 1};
 
-// Shared-memory copy of one table direction (rows in ascending column order).
-struct SmemTab {
-    int *ptr, *oth, *dir, *isd;
-    double *w;
-};
-
 // Block reduction of up to 3 per-thread values into partials (fixed tree).
 template <int NV>
 __device__ __forceinline__ void block_partials(double (&v)[NV], double *partials, const int *slots, long long slot_stride,
@@ -327,30 +321,6 @@ __global__ void __launch_bounds__(256) k_vec(int op, Geo g, double *y, const dou
     }
 }
 
-// fast fused x/r update with ||r||^2 partials (slot 3)
-__global__ void __launch_bounds__(256) k_xr(Geo g, double *__restrict__ x, double *__restrict__ r,
-                                            const double *__restrict__ p, const double *__restrict__ w, const State *st,
-                                            double *partials, long long slot_stride, int rb, int pst) {
-    if (stopped(st)) return;
-    const int kl = blockIdx.y;
-    const long long chunk = (g.plane + rb - 1) / rb;
-    const long long r0 = (long long)blockIdx.x * chunk;
-    const long long r1 = min(g.plane, r0 + chunk);
-    const long long base = (long long)kl * g.plane;
-    const double alpha = st->alpha;
-    double acc = 0.0;
-    for (long long rp = r0 + threadIdx.x; rp < r1; rp += blockDim.x) {
-        const long long i = base + rp;
-        x[i] = fma(alpha, p[i], x[i]);
-        double rv = fma(-alpha, w[i], r[i]);
-        r[i] = rv;
-        acc = fma(rv, rv, acc);
-    }
-    double v[1] = {acc};
-    const int sl[1] = {3};
-    block_partials<1>(v, partials, sl, slot_stride, (long long)(g.z0 + kl) * pst + blockIdx.x);
-}
-
 // fast r -= alpha w with ||r||^2 partials (slot 3); x is updated later,
 // fused with the p update (k_xp), with the same alpha and p (bitwise equal)
 __global__ void __launch_bounds__(256) k_r(Geo g, double *__restrict__ r, const double *__restrict__ w,
@@ -395,22 +365,6 @@ __global__ void __launch_bounds__(256) k_xp(Geo g, double *__restrict__ x, doubl
     }
 }
 
-// fast p = zt + beta p
-__global__ void __launch_bounds__(256) k_pupd(Geo g, double *__restrict__ p, const double *__restrict__ zt,
-                                              const State *st, int rb) {
-    if (stopped(st)) return;
-    const int kl = blockIdx.y;
-    const long long chunk = (g.plane + rb - 1) / rb;
-    const long long r0 = (long long)blockIdx.x * chunk;
-    const long long r1 = min(g.plane, r0 + chunk);
-    const long long base = (long long)kl * g.plane;
-    const double beta = st->beta;
-    for (long long rp = r0 + threadIdx.x; rp < r1; rp += blockDim.x) {
-        const long long i = base + rp;
-        p[i] = fma(beta, p[i], zt[i]);
-    }
-}
-
 // deterministic dot products into slot (per plane-block partials)
 __global__ void __launch_bounds__(256) k_dot(Geo g, const double *__restrict__ a, const double *__restrict__ b,
                                              int slot, double *partials, long long slot_stride, int rb,
@@ -436,15 +390,6 @@ int launch_vec(pn_context *c, int op, double *y, const double *a, const double *
     return PN_OK;
 }
 
-int launch_xr(pn_context *c, cudaStream_t s) {
-    dim3 grid(c->vec_bx, c->g.nzl);
-    k_xr<<<grid, 256, 0, s>>>(c->g, c->x.p, c->r.p, c->p.p, c->w.p, c->state, c->partials, slot_stride(c),
-                              c->vec_bx, c->red_bx);
-    PN_CUDA(cudaGetLastError());
-    c->launches++;
-    return PN_OK;
-}
-
 int launch_r_update(pn_context *c, cudaStream_t s) {
     dim3 grid(c->vec_bx, c->g.nzl);
     k_r<<<grid, 256, 0, s>>>(c->g, c->r.p, c->w.p, c->state, c->partials, slot_stride(c), c->vec_bx, c->red_bx);
@@ -456,14 +401,6 @@ int launch_r_update(pn_context *c, cudaStream_t s) {
 int launch_xp_update(pn_context *c, const double *zt, cudaStream_t s) {
     dim3 grid(c->vec_bx, c->g.nzl);
     k_xp<<<grid, 256, 0, s>>>(c->g, c->x.p, c->p.p, zt, c->state, c->vec_bx);
-    PN_CUDA(cudaGetLastError());
-    c->launches++;
-    return PN_OK;
-}
-
-int launch_pupd(pn_context *c, const double *zt, cudaStream_t s) {
-    dim3 grid(c->vec_bx, c->g.nzl);
-    k_pupd<<<grid, 256, 0, s>>>(c->g, c->p.p, zt, c->state, c->vec_bx);
     PN_CUDA(cudaGetLastError());
     c->launches++;
     return PN_OK;
