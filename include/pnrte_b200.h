@@ -78,6 +78,21 @@ int pn_create_csr(int64_t n, int64_t nnz, const int64_t *indptr, const int32_t *
 int pn_destroy(pn_context *ctx);
 const char *pn_last_error(void);
 
+/* Assemble a single-GPU stencil context (fields set) into an explicit
+ * device CSR system, exactly as assemble() builds it (solver.py:96-186):
+ * bc 0 = Dirichlet (dropped writes, pinned rows), 1 = Neumann (writes
+ * redirected to the nearest in-domain sample, solver.py:133-135,146-147;
+ * duplicates summed, columns ascending, explicit zeros kept, i.e.
+ * coo_matrix(...).tocsr() at solver.py:182-185).  Returns a new CSR context
+ * (pn_create_csr semantics) and, when rhs is non-NULL, writes Q (device
+ * buffer of R doubles; Neumann rows are not pinned). */
+int pn_assemble_csr(pn_context *ctx, int32_t bc, double *rhs, pn_context **out, void *stream);
+
+/* Download a CSR context's A in scipy layout into HOST buffers (the
+ * assembled system's A.indptr / A.indices / A.data).  NULL arrays: only
+ * *nnz is written. */
+int pn_csr_export(pn_context *csr, int64_t *nnz, int64_t *indptr, int32_t *indices, double *data);
+
 /* Field slot s (order of desc): kind 0 = absent (zero), 1 = uniform scalar,
  * 2 = array.  Arrays are the reference's [i,j,k] C-order global field
  * (z fastest) in DEVICE memory; the context transposes its slab (+1 plane).

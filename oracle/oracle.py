@@ -66,6 +66,7 @@ def lib():
         L.or_ddot.restype = ctypes.c_double
         L.or_ddot.argtypes = [ctypes.c_int64, P, P, ctypes.c_int, ctypes.c_int]
         L.or_csr.restype = ctypes.c_int64
+        L.or_csr_bc.restype = ctypes.c_int64
         L.or_cgnr.restype = ctypes.c_int
         _lib = L
     return _lib
@@ -96,7 +97,11 @@ def ddot(x, y, threads=8, kernel=0):
 
 
 class StencilOracle:
-    """Oracle for one (tables, spec) pair: setup, A/A^T, CSR, CGNR, unstagger."""
+    """Oracle for one (tables, spec) pair: setup, A/A^T, CSR, CGNR, unstagger.
+
+    Neumann specs (spec.bc == "neumann", solver.py:133-135,146-147): the RHS
+    is not pinned and A is the explicit CSR of or_csr_bc; products, Jacobi
+    diagonal and CGNR then run over that CSR (scipy / CsrOracle)."""
 
     def __init__(self, tables, spec):
         from paper_1807_00410_b200.program import field_slots, pack_tables
@@ -130,12 +135,18 @@ class StencilOracle:
         f.n, f.kind, f.scalar = len(names), _ptr(self._kind), _ptr(self._scalar)
         f.data = ctypes.cast(ptrs, P)
         self._f = f
+        self.neumann = getattr(spec, "bc", "dirichlet") == "neumann"
         self.diag = np.empty(self.R)
         self.rhs = np.empty(self.R)
-        lib().or_setup(ctypes.byref(self._t), ctypes.byref(self._f), _ptr(self.diag), _ptr(self.rhs))
+        lib().or_setup_bc(ctypes.byref(self._t), ctypes.byref(self._f), int(not self.neumann), _ptr(self.diag),
+                          _ptr(self.rhs))
+        self._csro = CsrOracle(self.csr()) if self.neumann else None
 
     def apply(self, x, transpose=False):
         x = np.ascontiguousarray(x, np.float64)
+        if self._csro is not None:
+            A = self._csro.A
+            return A.T @ x if transpose else A @ x
         y = np.empty(self.R)
         lib().or_apply(ctypes.byref(self._t), _ptr(self.diag), int(transpose), _ptr(x), _ptr(y))
         return y
@@ -143,14 +154,18 @@ class StencilOracle:
     def csr(self):
         import scipy.sparse as sp
         L = lib()
-        nnz = L.or_csr(ctypes.byref(self._t), _ptr(self.diag), None, None, None)
+        nm = int(self.neumann)
+        nnz = L.or_csr_bc(ctypes.byref(self._t), _ptr(self.diag), nm, None, None, None)
         indptr = np.empty(self.R + 1, np.int64)
         indices = np.empty(nnz, np.int32)
         data = np.empty(nnz)
-        L.or_csr(ctypes.byref(self._t), _ptr(self.diag), _ptr(indptr), _ptr(indices), _ptr(data))
+        L.or_csr_bc(ctypes.byref(self._t), _ptr(self.diag), nm, _ptr(indptr), _ptr(indices), _ptr(data))
         return sp.csr_matrix((data, indices, indptr), shape=(self.R, self.R))
 
     def jacobi_diag(self):
+        if self._csro is not None:
+            A = self._csro.A
+            return np.asarray(A.multiply(A).sum(axis=0)).ravel()
         out = np.empty(self.R)
         lib().or_jacobi_diag(ctypes.byref(self._t), _ptr(self.diag), _ptr(out))
         return out
@@ -167,6 +182,9 @@ class StencilOracle:
             blas_threads = th if blas_threads is None else blas_threads
             blas_kernel = kn if blas_kernel is None else blas_kernel
         b = self.rhs if b is None else np.ascontiguousarray(b, np.float64)
+        if self._csro is not None:
+            return self._csro.cgnr(b, tol=tol, max_iter=max_iter, primal_tol=primal_tol, jacobi=jacobi, x0=x0,
+                                   blas_threads=blas_threads, blas_kernel=blas_kernel)
         return _cgnr(self._op(), self.R, b, tol, max_iter, primal_tol, jacobi, x0,
                      blas_threads, blas_kernel, self.jacobi_diag if jacobi else None)
 

@@ -8,6 +8,9 @@
  *
  *   or_setup        diagonal + RHS of assemble()      solver.py:96-186, cas.py:465-517
  *   or_csr          the assembled CSR, scipy order     solver.py:129-185 (coo->csr)
+ *   or_csr_bc       same with the boundary condition: Neumann redirects
+ *                   writes into the domain (solver.py:133-135,146-147) and
+ *                   tocsr() sums the duplicates (solver.py:182-185)
  *   or_apply        y = A x / A^T x, scipy csr_matvec order (sequential,
  *                   ascending column, mul then add, no FMA)   solver.py:209,226-227,232,239
  *   or_jacobi_diag  colsum(A o A), ascending row order solver.py:218-223
@@ -87,7 +90,7 @@ static double eval_terms(const or_tables *T, const or_fields *F, int t0, int t1,
 }
 
 /* diag[R], rhs[R]; pinned rows keep their diagonal and get rhs 0 (solver.py:136-141,179-180) */
-void or_setup(const or_tables *T, const or_fields *F, double *diag, double *rhs) {
+void or_setup_bc(const or_tables *T, const or_fields *F, int pin, double *diag, double *rhs) {
     const int U = T->U;
     const int64_t nvox = (int64_t)T->nx * T->ny * T->nz;
 #pragma omp parallel for schedule(static)
@@ -98,10 +101,12 @@ void or_setup(const or_tables *T, const or_fields *F, double *diag, double *rhs)
             diag[v * U + c] = eval_terms(T, F, T->d_ptr[c], T->d_ptr[c + 1], i, j, k);
             double r = 0.0;
             if (T->r_ptr[c + 1] > T->r_ptr[c]) r = -eval_terms(T, F, T->r_ptr[c], T->r_ptr[c + 1], i, j, k);
-            rhs[v * U + c] = (T->par[c] & bb) ? 0.0 : r;
+            rhs[v * U + c] = (pin && (T->par[c] & bb)) ? 0.0 : r;
         }
     }
 }
+
+void or_setup(const or_tables *T, const or_fields *F, double *diag, double *rhs) { or_setup_bc(T, F, 1, diag, rhs); }
 
 /* neighbour voxel along direction code d, or -1 when outside the domain */
 static inline int64_t neighbour(const or_tables *T, int i, int j, int k, int d, int *bb) {
@@ -194,6 +199,55 @@ int64_t or_csr(const or_tables *T, const double *diag, int64_t *indptr, int32_t 
                     col = u * U + o; a = T->a_w[e];
                 }
                 if (indices) { indices[nnz] = (int32_t)col; data[nnz] = a; }
+                ++nnz;
+            }
+            if (indptr) indptr[v * U + c + 1] = nnz;
+        }
+    }
+    return nnz;
+}
+
+/*
+ * Neumann CSR: every entry of row (v, c) is written, its target index
+ * clipped into the domain; tocsr() then orders each row by column and sums
+ * entries that share one (sum_duplicates).  Per row: collect (col, value) in
+ * program order, stable insertion sort by column, sum equal neighbours left
+ * to right.  neumann = 0 gives or_csr.
+ */
+int64_t or_csr_bc(const or_tables *T, const double *diag, int neumann, int64_t *indptr, int32_t *indices,
+                  double *data) {
+    if (!neumann) return or_csr(T, diag, indptr, indices, data);
+    const int U = T->U;
+    const int64_t nvox = (int64_t)T->nx * T->ny * T->nz;
+    int64_t nnz = 0;
+    int64_t cols[256];
+    double vals[256];
+    if (indptr) indptr[0] = 0;
+    for (int64_t v = 0; v < nvox; ++v) {
+        int i = (int)(v % T->nx), j = (int)((v / T->nx) % T->ny), k = (int)(v / ((int64_t)T->nx * T->ny));
+        for (int c = 0; c < U; ++c) {
+            int n = 0;
+            for (int e = T->a_ptr[c]; e < T->a_ptr[c + 1]; ++e) {
+                int64_t col;
+                double a;
+                if (T->a_diag[e]) { col = v * U + c; a = diag[v * U + c]; }
+                else {
+                    int d = T->a_dir[e];
+                    int ii = i + DX[d], jj = j + DY[d], kk = k + DZ[d];
+                    ii = ii < 0 ? 0 : (ii >= T->nx ? T->nx - 1 : ii);
+                    jj = jj < 0 ? 0 : (jj >= T->ny ? T->ny - 1 : jj);
+                    kk = kk < 0 ? 0 : (kk >= T->nz ? T->nz - 1 : kk);
+                    col = ((int64_t)ii + (int64_t)T->nx * (jj + (int64_t)T->ny * kk)) * U + T->a_tgt[e];
+                    a = T->a_w[e];
+                }
+                int p = n;
+                while (p > 0 && cols[p - 1] > col) { cols[p] = cols[p - 1]; vals[p] = vals[p - 1]; --p; }
+                cols[p] = col; vals[p] = a; ++n;
+            }
+            for (int q = 0; q < n; ++q) {
+                double acc = vals[q];
+                while (q + 1 < n && cols[q + 1] == cols[q]) acc += vals[++q];
+                if (indices) { indices[nnz] = (int32_t)cols[q]; data[nnz] = acc; }
                 ++nnz;
             }
             if (indptr) indptr[v * U + c + 1] = nnz;

@@ -73,6 +73,8 @@ def load():
         "pn_create": [ctypes.POINTER(Desc), ctypes.POINTER(P)],
         "pn_create_csr": [I64, I64, P, P, P, I32, ctypes.POINTER(P)],
         "pn_destroy": [P],
+        "pn_assemble_csr": [P, I32, P, ctypes.POINTER(P), P],
+        "pn_csr_export": [P, ctypes.POINTER(I64), P, P, P],
         "pn_set_field": [P, I32, I32, F64, P, P],
         "pn_setup": [P, P],
         "pn_export_diag_rhs": [P, P, P, P],

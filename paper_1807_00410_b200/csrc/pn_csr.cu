@@ -6,6 +6,10 @@
 // built on the device exactly like A.T.tocsr() (solver.py:203): a stable sort
 // of the entries by column keeps, inside every transposed row, ascending
 // original row order and stored order among duplicates.
+// Stencil systems can also be assembled into this form on the device
+// (k_stencil_csr): the export behind StencilOperator.to_scipy() and the
+// operator of Neumann-boundary systems, whose redirected writes the
+// matrix-free kernels do not model.
 // This file is compiled with -fmad=false (faithful sums are mul-then-add).
 #include <cuda_runtime.h>
 
@@ -101,10 +105,11 @@ int csr_build(pn_context *c, long long n, long long nnz, const long long *h_ap, 
     PN_CUDA(cudaMalloc(&o.tp, (n + 1) * sizeof(long long)));
     PN_CUDA(cudaMalloc(&o.tj, std::max<long long>(nnz, 1) * sizeof(int)));
     PN_CUDA(cudaMalloc(&o.tx, std::max<long long>(nnz, 1) * sizeof(double)));
-    PN_CUDA(cudaMemcpy(o.ap, h_ap, (n + 1) * sizeof(long long), cudaMemcpyHostToDevice));
+    // host or device sources (unified addressing decides the direction)
+    PN_CUDA(cudaMemcpy(o.ap, h_ap, (n + 1) * sizeof(long long), cudaMemcpyDefault));
     if (nnz) {
-        PN_CUDA(cudaMemcpy(o.aj, h_aj, nnz * sizeof(int), cudaMemcpyHostToDevice));
-        PN_CUDA(cudaMemcpy(o.ax, h_ax, nnz * sizeof(double), cudaMemcpyHostToDevice));
+        PN_CUDA(cudaMemcpy(o.aj, h_aj, nnz * sizeof(int), cudaMemcpyDefault));
+        PN_CUDA(cudaMemcpy(o.ax, h_ax, nnz * sizeof(double), cudaMemcpyDefault));
     }
     PN_CUDA(cudaMemset(o.tp, 0, (n + 1) * sizeof(long long)));
     if (nnz == 0) return PN_OK;
@@ -136,6 +141,111 @@ int csr_build(pn_context *c, long long n, long long nnz, const long long *h_ap, 
     PN_CUDA(cudaDeviceSynchronize());
     cudaFree(k_in); cudaFree(k_out); cudaFree(v_in); cudaFree(v_out); cudaFree(cnt); cudaFree(tmp); cudaFree(stmp);
     return PN_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Device assembly (solver.py:96-186).  One thread per row (v, c): walk the
+// row's table entries in program order, map each to its column -- Dirichlet:
+// dropped when the target is outside the domain, on the last face sample of
+// its staggered axis, or the row is pinned (:151-163); Neumann: target index
+// clipped into the domain (:146-147) -- and insert it into a per-row sorted
+// list, summing entries that land on the same column.  The result is
+// coo_matrix(...).tocsr(): ascending columns, duplicates summed (a row sees
+// at most two writes per column -- a staggered target is reached along one
+// axis only -- so the sum is order independent), explicit zeros kept.
+// Pass 1 (ap == nullptr) writes per-row counts, pass 2 fills.
+__constant__ int a_dx[7] = {0, -1, 1, 0, 0, 0, 0};
+__constant__ int a_dy[7] = {0, 0, 0, -1, 1, 0, 0};
+__constant__ int a_dz[7] = {0, 0, 0, 0, 0, -1, 1};
+
+__global__ void k_stencil_csr(Tables T, Geo g, const double *__restrict__ diag, int neumann, long long *cnt,
+                              const long long *__restrict__ ap, int *aj, double *ax) {
+    const long long row = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long R = (long long)g.nz * g.plane;
+    if (row >= R) return;
+    const int U = g.U;
+    const long long v = row / U;
+    const int c = (int)(row - v * U);
+    const int i = (int)(v % g.nx), j = (int)((v / g.nx) % g.ny), k = (int)(v / g.pvox);
+    const int bb = (i == g.nx - 1) | ((j == g.ny - 1) << 1) | ((k == g.nz - 1) << 2);
+    const bool pinned = !neumann && (T.par[c] & bb);
+    int col[ASM_MAX];
+    double val[ASM_MAX];
+    int n = 0;
+    for (int e = T.a_ptr[c]; e < T.a_ptr[c + 1]; ++e) {
+        int cc;
+        double a;
+        if (T.a_diag[e]) {
+            cc = (int)row;
+            a = diag[row];
+        } else {
+            const int o = T.a_tgt[e], d = T.a_dir[e];
+            int ii = i + a_dx[d], jj = j + a_dy[d], kk = k + a_dz[d];
+            if (neumann) {
+                ii = min(max(ii, 0), g.nx - 1);
+                jj = min(max(jj, 0), g.ny - 1);
+                kk = min(max(kk, 0), g.nz - 1);
+            } else {
+                if (pinned || ii < 0 || jj < 0 || kk < 0 || ii >= g.nx || jj >= g.ny || kk >= g.nz) continue;
+                const int nbb = (ii == g.nx - 1) | ((jj == g.ny - 1) << 1) | ((kk == g.nz - 1) << 2);
+                if (T.par[o] & nbb) continue;
+            }
+            cc = (int)(((long long)kk * g.pvox + (long long)jj * g.nx + ii) * U + o);
+            a = T.a_w[e];
+        }
+        int p = n;
+        while (p > 0 && col[p - 1] > cc) --p;
+        if (p > 0 && col[p - 1] == cc) {
+            val[p - 1] = __dadd_rn(val[p - 1], a);
+            continue;
+        }
+        for (int q = n; q > p; --q) { col[q] = col[q - 1]; val[q] = val[q - 1]; }
+        col[p] = cc;
+        val[p] = a;
+        ++n;
+    }
+    if (!ap) {
+        cnt[row] = n;
+        return;
+    }
+    const long long base = ap[row];
+    for (int q = 0; q < n; ++q) { aj[base + q] = col[q]; ax[base + q] = val[q]; }
+}
+
+int stencil_csr_assemble(pn_context *c, int neumann, cudaStream_t s, long long **ap_out, int **aj_out,
+                         double **ax_out, long long *nnz_out) {
+    const Geo &g = c->g;
+    const long long R = (long long)g.nz * g.plane;
+    long long *cnt = nullptr, *ap = nullptr;
+    int *aj = nullptr;
+    double *ax = nullptr;
+    void *tmp = nullptr;
+    size_t tmp_bytes = 0;
+    long long nnz = 0;
+    const unsigned nb = (unsigned)((R + 127) / 128);
+    int st = PN_OK;
+    auto fail = [&](int code) { cudaFree(cnt); cudaFree(ap); cudaFree(aj); cudaFree(ax); cudaFree(tmp); return code; };
+    if (cudaMalloc(&cnt, (R + 1) * 8) != cudaSuccess || cudaMalloc(&ap, (R + 1) * 8) != cudaSuccess)
+        return fail(PN_ERR_NOMEM);
+    if (cudaMemsetAsync(cnt, 0, (R + 1) * 8, s) != cudaSuccess) return fail(PN_ERR_CUDA);
+    k_stencil_csr<<<nb, 128, 0, s>>>(c->tb, g, c->diag, neumann, cnt, nullptr, nullptr, nullptr);
+    if (cudaGetLastError() != cudaSuccess) return fail(PN_ERR_CUDA);
+    cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, cnt, ap, (int)(R + 1), s);
+    if (cudaMalloc(&tmp, std::max<size_t>(tmp_bytes, 1)) != cudaSuccess) return fail(PN_ERR_NOMEM);
+    if (cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt, ap, (int)(R + 1), s) != cudaSuccess) return fail(PN_ERR_CUDA);
+    if (cudaMemcpyAsync(&nnz, ap + R, 8, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess)
+        return fail(PN_ERR_CUDA);
+    if (cudaMalloc(&aj, std::max<long long>(nnz, 1) * sizeof(int)) != cudaSuccess ||
+        cudaMalloc(&ax, std::max<long long>(nnz, 1) * sizeof(double)) != cudaSuccess)
+        return fail(PN_ERR_NOMEM);
+    k_stencil_csr<<<nb, 128, 0, s>>>(c->tb, g, c->diag, neumann, nullptr, ap, aj, ax);
+    if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(s) != cudaSuccess) return fail(PN_ERR_CUDA);
+    c->launches += 2;
+    cudaFree(cnt);
+    cudaFree(tmp);
+    *ap_out = ap; *aj_out = aj; *ax_out = ax; *nnz_out = nnz;
+    return st;
 }
 
 void csr_release(pn_context *c) {

@@ -163,7 +163,7 @@ namespace pn {
 // kernels (pn_kernels.cu)
 int launch_fill(double *p, long long n, double v, cudaStream_t s);
 int launch_field_slab(pn_context *c, int slot, const double *src, double *dst, cudaStream_t s);
-int launch_setup(pn_context *c, bool want_diag, bool want_rhs, cudaStream_t s);
+int launch_setup(pn_context *c, bool want_diag, bool want_rhs, cudaStream_t s, double *rhs_out = nullptr, int pin = 1);
 int launch_apply_table(pn_context *c, int trans, int faithful, int squared, const double *x, double *y, int red,
                        const double *minv, double *zt, cudaStream_t s, bool gated, int kl0 = 0, int npl = -1,
                        int kst = 1);
@@ -179,6 +179,11 @@ int launch_unstagger(pn_context *c, const double *u, double *out, cudaStream_t s
 
 // generic CSR (pn_csr.cu)
 int csr_build(pn_context *c, long long n, long long nnz, const long long *ap, const int *aj, const double *ax);
+// device assembly of a stencil context into canonical CSR (caller frees);
+// rows may hold at most ASM_MAX table entries (P7: 21)
+constexpr int ASM_MAX = 48;
+int stencil_csr_assemble(pn_context *c, int neumann, cudaStream_t s, long long **ap, int **aj, double **ax,
+                         long long *nnz);
 void csr_release(pn_context *c);
 int launch_csr_apply(pn_context *c, int trans, int faithful, int squared, const double *x, double *y, int red,
                      const double *minv, double *zt, cudaStream_t s, bool gated);

@@ -92,8 +92,9 @@ __device__ __forceinline__ int boundary_bits(const Geo &g, int i, int j, int kg)
     return (i == g.nx - 1) | ((j == g.ny - 1) << 1) | ((kg == g.nz - 1) << 2);
 }
 
-// one thread per (local voxel, comp): diag (optional) and RHS (solver.py:136-181)
-__global__ void k_setup(Tables T, Fields F, Geo g, double *diag, double *rhs) {
+// one thread per (local voxel, comp): diag (optional) and RHS (solver.py:136-181);
+// pin = 0 for Neumann (no pinned rows, solver.py:133-135)
+__global__ void k_setup(Tables T, Fields F, Geo g, double *diag, double *rhs, int pin) {
     long long row = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     long long R = (long long)g.nzl * g.plane;
     if (row >= R) return;
@@ -107,15 +108,16 @@ __global__ void k_setup(Tables T, Fields F, Geo g, double *diag, double *rhs) {
     if (rhs) {
         double r = 0.0;
         if (T.r_ptr[c + 1] > T.r_ptr[c]) r = -eval_terms(T, F, g, T.r_ptr[c], T.r_ptr[c + 1], i, j, kl);
-        rhs[row] = (T.par[c] & bb) ? 0.0 : r;
+        rhs[row] = (pin && (T.par[c] & bb)) ? 0.0 : r;
     }
 }
 
-int launch_setup(pn_context *c, bool want_diag, bool want_rhs, cudaStream_t s) {
+int launch_setup(pn_context *c, bool want_diag, bool want_rhs, cudaStream_t s, double *rhs_out, int pin) {
     long long R = c->R_l();
     int bs = 256;
     long long nb = (R + bs - 1) / bs;
-    k_setup<<<(unsigned)nb, bs, 0, s>>>(c->tb, c->f, c->g, want_diag ? c->diag : nullptr, want_rhs ? c->b.p : nullptr);
+    double *rhs = want_rhs ? (rhs_out ? rhs_out : c->b.p) : nullptr;
+    k_setup<<<(unsigned)nb, bs, 0, s>>>(c->tb, c->f, c->g, want_diag ? c->diag : nullptr, rhs, pin);
     PN_CUDA(cudaGetLastError());
     c->launches++;
     return PN_OK;

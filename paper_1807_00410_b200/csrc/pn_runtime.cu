@@ -248,15 +248,8 @@ int pn_create(const pn_desc *d, pn_context **out) {
     return PN_OK;
 }
 
-int pn_create_csr(int64_t n, int64_t nnz, const int64_t *indptr, const int32_t *indices, const double *data,
-                  int32_t device, pn_context **out) {
-    if (!out || n < 1 || nnz < 0 || !indptr || (nnz && (!indices || !data))) {
-        set_error("invalid CSR arguments");
-        return PN_ERR_INVALID;
-    }
-    if (indptr[0] != 0 || indptr[n] != nnz) { set_error("indptr does not span nnz"); return PN_ERR_INVALID; }
-    for (int64_t e = 0; e < nnz; ++e)
-        if (indices[e] < 0 || indices[e] >= n) { set_error("column index out of range"); return PN_ERR_INVALID; }
+static int create_csr_ctx(int64_t n, int64_t nnz, const int64_t *indptr, const int32_t *indices,
+                          const double *data, int32_t device, pn_context **out) {
     PN_CUDA(cudaSetDevice(device));
     pn_context *c = new pn_context();
     c->is_csr = true;
@@ -280,6 +273,57 @@ int pn_create_csr(int64_t n, int64_t nnz, const int64_t *indptr, const int32_t *
     if (st != PN_OK) { pn_destroy(c); return st; }
     c->setup_done = true;
     *out = c;
+    return PN_OK;
+}
+
+int pn_create_csr(int64_t n, int64_t nnz, const int64_t *indptr, const int32_t *indices, const double *data,
+                  int32_t device, pn_context **out) {
+    if (!out || n < 1 || nnz < 0 || !indptr || (nnz && (!indices || !data))) {
+        set_error("invalid CSR arguments");
+        return PN_ERR_INVALID;
+    }
+    if (indptr[0] != 0 || indptr[n] != nnz) { set_error("indptr does not span nnz"); return PN_ERR_INVALID; }
+    for (int64_t e = 0; e < nnz; ++e)
+        if (indices[e] < 0 || indices[e] >= n) { set_error("column index out of range"); return PN_ERR_INVALID; }
+    return create_csr_ctx(n, nnz, indptr, indices, data, device, out);
+}
+
+int pn_assemble_csr(pn_context *c, int32_t bc, double *rhs, pn_context **out, void *stream) {
+    if (!c || !out || (bc != 0 && bc != 1)) { set_error("invalid arguments"); return PN_ERR_INVALID; }
+    if (c->is_csr) { set_error("context is already a CSR system"); return PN_ERR_UNSUPPORTED; }
+    if (c->world != 1) { set_error("CSR assembly is single-GPU (one slab)"); return PN_ERR_UNSUPPORTED; }
+    if (!c->setup_done) { set_error("fields not set (pn_setup)"); return PN_ERR_INVALID; }
+    const long long R = c->R_l();
+    if (R >= (1LL << 31)) { set_error("system too large for 32-bit CSR indices"); return PN_ERR_UNSUPPORTED; }
+    PN_CUDA(cudaSetDevice(c->device));
+    {
+        std::vector<int> ptr(c->U + 1);
+        PN_CUDA(cudaMemcpy(ptr.data(), c->tb.a_ptr, (c->U + 1) * sizeof(int), cudaMemcpyDeviceToHost));
+        for (int q = 0; q < c->U; ++q)
+            if (ptr[q + 1] - ptr[q] > ASM_MAX) { set_error("stencil row too long for CSR assembly"); return PN_ERR_UNSUPPORTED; }
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    PN_TRY(ensure_diag(c, s));
+    if (rhs) PN_TRY(launch_setup(c, false, true, s, rhs, bc == 0 ? 1 : 0));
+    long long *ap;
+    int *aj;
+    double *ax;
+    long long nnz;
+    PN_TRY(stencil_csr_assemble(c, bc, s, &ap, &aj, &ax, &nnz));
+    int st = create_csr_ctx(R, nnz, (const int64_t *)ap, aj, ax, c->device, out);
+    cudaFree(ap); cudaFree(aj); cudaFree(ax);
+    return st;
+}
+
+int pn_csr_export(pn_context *c, int64_t *nnz, int64_t *indptr, int32_t *indices, double *data) {
+    if (!c || !nnz) { set_error("invalid arguments"); return PN_ERR_INVALID; }
+    if (!c->is_csr) { set_error("not a CSR context (pn_assemble_csr first)"); return PN_ERR_UNSUPPORTED; }
+    PN_CUDA(cudaSetDevice(c->device));
+    const CsrOp &o = c->csr;
+    *nnz = o.nnz;
+    if (indptr) PN_CUDA(cudaMemcpy(indptr, o.ap, (o.n + 1) * 8, cudaMemcpyDeviceToHost));
+    if (indices && o.nnz) PN_CUDA(cudaMemcpy(indices, o.aj, o.nnz * sizeof(int), cudaMemcpyDeviceToHost));
+    if (data && o.nnz) PN_CUDA(cudaMemcpy(data, o.ax, o.nnz * sizeof(double), cudaMemcpyDeviceToHost));
     return PN_OK;
 }
 

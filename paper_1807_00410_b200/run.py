@@ -51,6 +51,7 @@ class RunConfig:
     seed: int = 0
     jacobi: bool = False
     mode: str = "fast"            # fast | faithful
+    bc: str = ""                  # '' = problem default | dirichlet | neumann (cli.py:46,105-107)
     device: int = 0
 
     def validated(self):
@@ -66,6 +67,8 @@ class RunConfig:
             raise ConfigError("max-iter must be >= 1")
         if self.mode not in ("fast", "faithful"):
             raise ConfigError(f"unknown mode {self.mode!r}")
+        if self.bc and self.bc not in ("dirichlet", "neumann"):
+            raise ConfigError(f"unknown bc {self.bc!r}")
         return self
 
 
@@ -126,6 +129,8 @@ def build_problem(cfg):
     tau = cfg.floor if cfg.floor > 0 else floor
     if tau:
         spec = floor_sigma_t(spec, tau)
+    if cfg.bc:
+        spec = replace(spec, bc=cfg.bc)
     return spec
 
 
@@ -152,8 +157,13 @@ def run(cfg, log=print):
     ctx = PnContext(tables, spec.res, spec.h, device=cfg.device)
     ctx.set_fields(spec)
     R = ctx.R_local
-    log(f"assembled {R} rows on cuda:{cfg.device} (matrix-free P{cfg.order} stencil)")
-    x, report = ctx.solve(tol=cfg.tol, max_iter=cfg.max_iter, jacobi=cfg.jacobi, mode=cfg.mode)
+    if spec.bc == "neumann":
+        op, b = ctx.assemble_csr("neumann")
+        log(f"assembled {R} rows on cuda:{cfg.device} (P{cfg.order}, Neumann: explicit device CSR)")
+    else:
+        op, b = ctx, None
+        log(f"assembled {R} rows on cuda:{cfg.device} (matrix-free P{cfg.order} stencil)")
+    x, report = op.solve(tol=cfg.tol, max_iter=cfg.max_iter, jacobi=cfg.jacobi, mode=cfg.mode, b=b)
     log(f"solve: {report.iterations} iterations, converged={report.converged}, "
         f"normal={report.normal_residual:.3e}, primal={report.primal_residual:.3e}, "
         f"wall={report.wall_time:.2f}s")
@@ -162,7 +172,7 @@ def run(cfg, log=print):
     r, line = center_profile(spec, coll)
     fio.write_profile(os.path.join(cfg.out, "profile.csv"), zip(r, line))
     with open(os.path.join(cfg.out, "solve.log"), "w") as fh:
-        fh.write(f"rows {R}\nmode {cfg.mode}\n")
+        fh.write(f"rows {R}\nmode {cfg.mode}\nbc {spec.bc}\n")
         fh.write(f"iterations {report.iterations}\nconverged {report.converged}\n")
         fh.write(f"normal_residual {report.normal_residual!r}\nprimal_residual {report.primal_residual!r}\n")
         fh.write(f"wall_time {report.wall_time!r}\n# iter normal primal\n")

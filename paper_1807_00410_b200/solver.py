@@ -13,7 +13,8 @@ for tol <= 0 or a dim mismatch, non-convergence reported in the report, zero
 RHS returns x = 0 converged).  ``assemble`` does not build a CSR matrix: it
 creates a device context holding the stencil tables and the fields, and the
 system's ``A`` is a matrix-free operator (``A @ x``, ``A.T @ x`` run the sm_100a
-kernels; ``A.to_scipy()`` exports the exact CSR for parity checks).
+kernels; ``A.to_scipy()`` exports the exact CSR, assembled on the device, for
+parity checks).  Neumann specs get an explicit device CSR (CsrOperator).
 
 Extra keyword arguments (all optional): ``mode`` ("fast" | "faithful"),
 ``device`` and, for faithful runs, ``blas_threads`` / ``blas_kernel`` (the
@@ -41,7 +42,7 @@ SQRT_4PI = math.sqrt(4.0 * math.pi)
 
 @dataclass(frozen=True)
 class SparseSystem:
-    A: object               # StencilOperator (matrix-free, device)
+    A: object               # StencilOperator (matrix-free) or CsrOperator, on the device
     Q: np.ndarray
     res: tuple
     n_unknowns: int
@@ -134,35 +135,72 @@ class PnContext:
         self._torch = torch
 
     @classmethod
+    def _csr_shell(cls, n, device):
+        self = cls.__new__(cls)
+        self.tables = None
+        self.dim = 1
+        self.N, self.U = 0, 1
+        self.res = (int(n), 1, 1)
+        self.h = 1.0
+        self.device = int(device)
+        self.z0, self.nz_local = 0, 1
+        self.R_local = int(n)
+        self.pk = None
+        self._L = _lib.load()
+        self._torch = _torch()
+        return self
+
+    @classmethod
     def from_csr(cls, A, device=0):
         """Device context of a generic sparse system (any SparseSystem.A)."""
         import scipy.sparse as sp
-        torch = _torch()
-        L = _lib.load()
         A = sp.csr_matrix(A)
         if A.shape[0] != A.shape[1]:
             raise ValueError("system matrix must be square")
         indptr = np.ascontiguousarray(A.indptr, dtype=np.int64)
         indices = np.ascontiguousarray(A.indices, dtype=np.int32)
         data = np.ascontiguousarray(A.data, dtype=np.float64)
-        self = cls.__new__(cls)
-        self.tables = None
-        self.dim = 1
-        self.N, self.U = 0, 1
-        self.res = (A.shape[0], 1, 1)
-        self.h = 1.0
-        self.device = int(device)
-        self.z0, self.nz_local = 0, 1
-        self.R_local = A.shape[0]
-        self.pk = None
+        self = cls._csr_shell(A.shape[0], device)
+        handle = ctypes.c_void_p()
+        with self._torch.cuda.device(self.device):
+            _lib.check(self._L.pn_create_csr(A.shape[0], len(data), indptr.ctypes.data, indices.ctypes.data,
+                                             data.ctypes.data, self.device, ctypes.byref(handle)))
+        self.handle = handle
+        return self
+
+    @property
+    def is_csr(self):
+        return self.tables is None
+
+    def assemble_csr(self, bc="dirichlet"):
+        """Explicit device CSR of this stencil system (pn_assemble_csr): the
+        CSR context and the RHS Q (device tensor).  bc "neumann" redirects
+        writes into the domain (solver.py:146-147) and leaves rows unpinned."""
+        if bc not in ("dirichlet", "neumann"):
+            raise ValueError(f"unknown boundary condition {bc!r}")
+        torch = self._torch
+        q = self.empty()
         handle = ctypes.c_void_p()
         with torch.cuda.device(self.device):
-            _lib.check(L.pn_create_csr(A.shape[0], len(data), indptr.ctypes.data, indices.ctypes.data,
-                                       data.ctypes.data, self.device, ctypes.byref(handle)))
-        self.handle = handle
-        self._L = L
-        self._torch = torch
-        return self
+            _lib.check(self._L.pn_assemble_csr(self.handle, 1 if bc == "neumann" else 0, ctypes.c_void_p(q.data_ptr()),
+                                               ctypes.byref(handle), _stream(torch)))
+        csr = PnContext._csr_shell(self.R_local, self.device)
+        csr.handle = handle
+        return csr, q
+
+    def csr_export(self):
+        """A of a CSR context as a scipy matrix (pn_csr_export)."""
+        import scipy.sparse as sp
+        nnz = ctypes.c_int64()
+        _lib.check(self._L.pn_csr_export(self.handle, ctypes.byref(nnz), None, None, None))
+        indptr = np.empty(self.R_local + 1, np.int64)
+        indices = np.empty(nnz.value, np.int32)
+        data = np.empty(nnz.value)
+        with self._torch.cuda.device(self.device):
+            _lib.check(self._L.pn_csr_export(self.handle, ctypes.byref(nnz), indptr.ctypes.data_as(ctypes.c_void_p),
+                                             indices.ctypes.data_as(ctypes.c_void_p),
+                                             data.ctypes.data_as(ctypes.c_void_p)))
+        return sp.csr_matrix((data, indices, indptr), shape=(self.R_local, self.R_local))
 
     def __del__(self):
         h = getattr(self, "handle", None)
@@ -299,45 +337,20 @@ class StencilOperator:
         return self.matvec(x)
 
     def to_scipy(self):
-        """Exact CSR of A as the reference assembles it (debug / parity)."""
-        import scipy.sparse as sp
+        """Exact CSR of A (or A^T) as the reference assembles it, built on the
+        device (pn_assemble_csr) and downloaded -- debug / parity export."""
         ctx = self.ctx
-        diag = ctx.diag_rhs()[0].cpu().numpy()
-        A = _csr_from_tables(ctx.pk, ctx.res, diag)
+        A = ctx.csr_export() if ctx.is_csr else ctx.assemble_csr("dirichlet")[0].csr_export()
         return A.T.tocsr() if self.transpose else A
 
 
-def _csr_from_tables(pk, res, diag):
-    """Host-side CSR from the packed tables + device diagonal (vectorised
-    numpy; used only for exports / parity, not by the solve)."""
-    import scipy.sparse as sp
-    nx, ny, nz = res
-    U = pk["U"]
-    par = pk["par"]
-    v = np.arange(nx * ny * nz)
-    i, j, k = v % nx, (v // nx) % ny, v // (nx * ny)
-    bb = (i == nx - 1).astype(np.int32) | ((j == ny - 1).astype(np.int32) << 1) | ((k == nz - 1).astype(np.int32) << 2)
-    D = {0: (0, 0, 0), 1: (-1, 0, 0), 2: (1, 0, 0), 3: (0, -1, 0), 4: (0, 1, 0), 5: (0, 0, -1), 6: (0, 0, 1)}
-    rows, cols, vals = [], [], []
-    for c in range(U):
-        pinned_c = (par[c] & bb) != 0
-        for e in range(pk["a_ptr"][c], pk["a_ptr"][c + 1]):
-            t = pk["a_tgt"][e]
-            if pk["a_diag"][e]:
-                rows.append(v * U + c); cols.append(v * U + c); vals.append(diag[v * U + c])
-                continue
-            dx, dy, dz = D[int(pk["a_dir"][e])]
-            ii, jj, kk = i + dx, j + dy, k + dz
-            ok = (ii >= 0) & (jj >= 0) & (kk >= 0) & (ii < nx) & (jj < ny) & (kk < nz) & ~pinned_c
-            nbb = (ii == nx - 1).astype(np.int32) | ((jj == ny - 1).astype(np.int32) << 1) | \
-                ((kk == nz - 1).astype(np.int32) << 2)
-            ok &= (par[t] & nbb) == 0
-            u = ii + nx * (jj + ny * kk)
-            rows.append((v * U + c)[ok]); cols.append((u * U + t)[ok]); vals.append(np.full(ok.sum(), pk["a_w"][e]))
-    R = nx * ny * nz * U
-    A = sp.coo_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))), shape=(R, R)).tocsr()
-    A.sort_indices()
-    return A
+class CsrOperator(StencilOperator):
+    """Explicit device CSR A (or A^T): Neumann systems and generic sparse
+    systems.  Same ``@`` / ``.T`` / ``to_scipy()`` surface."""
+
+    @property
+    def T(self):
+        return CsrOperator(self.ctx, not self.transpose)
 
 
 def _check_dim(program, spec):
@@ -348,15 +361,26 @@ def _check_dim(program, spec):
         raise ValueError(f"problem is {len(tuple(spec.res))}-D but program is {dim}-D")
 
 
+def _bc(spec):
+    bc = getattr(spec, "bc", "dirichlet")
+    if bc not in ("dirichlet", "neumann"):
+        raise ValueError(f"unknown boundary condition {bc!r}")
+    return bc
+
+
 def assemble(program, spec, device=0):
     """Upload the stencil tables and fields and evaluate diagonal + RHS on the
-    device (solver.py:96-186).  Returns a SparseSystem whose A is matrix-free."""
+    device (solver.py:96-186).  Dirichlet: A is matrix-free.  Neumann: the
+    redirected writes are assembled into an explicit device CSR (same
+    entries as the reference's coo->csr), A is a CsrOperator over it."""
     _check_dim(program, spec)
-    if getattr(spec, "bc", "dirichlet") != "dirichlet":
-        raise NotImplementedError("matrix-free path implements vacuum (Dirichlet) boundaries")
+    bc = _bc(spec)
     tables = as_tables(program)
     ctx = PnContext(tables, spec.res, spec.h, device=device)
     ctx.set_fields(spec)
+    if bc == "neumann":
+        csr, q = ctx.assemble_csr("neumann")
+        return SparseSystem(A=CsrOperator(csr), Q=q.cpu().numpy(), res=tuple(spec.res), n_unknowns=tables.U)
     Q = ctx.diag_rhs()[1].cpu().numpy()
     return SparseSystem(A=StencilOperator(ctx), Q=Q, res=tuple(spec.res), n_unknowns=tables.U)
 
@@ -400,11 +424,17 @@ def solve_pn(program_or_N, spec, tol=1e-8, max_iter=50000, primal_tol=None, jaco
     coefficients per voxel out (cli.py:136-155 without file I/O)."""
     tables = as_tables(program_or_N)
     _check_dim(tables, spec)
+    bc = _bc(spec)
     ctx = PnContext(tables, spec.res, spec.h, device=device)
     ctx.set_fields(spec)
     if tol <= 0:
         raise ValueError("tolerance must be positive")
-    x, rep = ctx.solve(tol=tol, max_iter=max_iter, primal_tol=primal_tol, jacobi=jacobi, x0=x0, mode=mode, **kw)
+    if bc == "neumann":
+        csr, q = ctx.assemble_csr("neumann")
+        x, rep = csr.solve(tol=tol, max_iter=max_iter, primal_tol=primal_tol, jacobi=jacobi, x0=x0, b=q, mode=mode,
+                           **kw)
+    else:
+        x, rep = ctx.solve(tol=tol, max_iter=max_iter, primal_tol=primal_tol, jacobi=jacobi, x0=x0, mode=mode, **kw)
     coll = ctx.unstagger(x).cpu().numpy()
     if return_staggered:
         return coll, rep, x.cpu().numpy()

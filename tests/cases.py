@@ -38,6 +38,20 @@ CASES_2D = [
 ]
 
 
+# Neumann boundaries (bc="neumann": writes redirected into the domain,
+# solver.py:133-135,146-147), served by the device CSR assembly
+CASES_NEUMANN = [
+    ("n_p1_567", 1, (5, 6, 7), 41),
+    ("n_p2_445", 2, (4, 4, 5), 42),
+    ("n_p3_3245", 3, (32, 4, 5), 43),
+    ("n_p5_345", 5, (3, 4, 5), 44),
+    ("n_p7_343", 7, (3, 4, 3), 45),
+    ("n_p1_111", 1, (1, 1, 1), 46),
+]
+CASES_NEUMANN_2D = [("ncb_p2_15", 2, 15), ("ncb_p3_21", 3, 21)]
+NEUMANN_CASES = [c[0] for c in CASES_NEUMANN] + [c[0] for c in CASES_NEUMANN_2D]
+
+
 def tables_2d(N):
     import json
     import pathlib
@@ -83,4 +97,11 @@ def case_inputs(name):
     for cname, N, n in CASES_2D:
         if cname == name:
             return tables_2d(N), make_checkerboard(n)
+    from dataclasses import replace
+    for cname, N, res, seed in CASES_NEUMANN:
+        if cname == name:
+            return build_tables(N), replace(rand_spec(N, res, seed), bc="neumann")
+    for cname, N, n in CASES_NEUMANN_2D:
+        if cname == name:
+            return tables_2d(N), replace(make_checkerboard(n), bc="neumann")
     raise KeyError(name)

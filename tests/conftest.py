@@ -43,5 +43,7 @@ def golden():
         "cases": np.load(g / "cases.npz"),
         "cases_meta": json.loads((g / "cases.json").read_text()),
         "configs": json.loads((g / "configs.json").read_text()),
+        "neumann": np.load(g / "neumann.npz"),
+        "neumann_meta": json.loads((g / "neumann.json").read_text()),
         "dir": g,
     }

@@ -54,7 +54,8 @@ def test_profile_and_config_files(tmp_path):
 
 
 @pytest.mark.parametrize("mapping", [{"problem": "checkerboard"}, {"method": "cda"}, {"order": 0},
-                                     {"tol": 0}, {"bogus": 1}, {"jacobi": "maybe"}, {"mode": "turbo"}])
+                                     {"tol": 0}, {"bogus": 1}, {"jacobi": "maybe"}, {"mode": "turbo"},
+                                     {"bc": "periodic"}])
 def test_config_errors(mapping):
     with pytest.raises((ConfigError, ValueError)):
         config_from_mapping(mapping)

@@ -6,7 +6,7 @@ import hashlib
 import numpy as np
 import pytest
 
-from cases import ALL_CASES, CASES, case_inputs, probe_vector, rand_spec
+from cases import ALL_CASES, CASES, NEUMANN_CASES, case_inputs, probe_vector, rand_spec
 from oracle.oracle import StencilOracle, ddot
 from paper_1807_00410_b200.configs import make_config
 from paper_1807_00410_b200.program import build_tables
@@ -107,3 +107,47 @@ def test_oracle_matches_live_reference(case, ref):
     x, rep = o.cgnr(tol=1e-10, max_iter=500, jacobi=True)
     xr, rr = solve_normal_cg(s, tol=1e-10, max_iter=500, jacobi=True)
     assert rep["iterations"] == rr.iterations and x.tobytes() == xr.tobytes()
+
+
+# ---------------------------------------------------------------- Neumann --
+@pytest.mark.parametrize("case", NEUMANN_CASES)
+def test_oracle_neumann_matches_golden(case, golden):
+    """or_csr_bc / or_setup_bc against the reference's bc="neumann" assembly:
+    clipped writes, summed duplicates, unpinned RHS; CGNR over that CSR."""
+    o = StencilOracle(*case_inputs(case))
+    g, meta = golden["neumann"], golden["neumann_meta"]["cases"][case]
+    A = o.csr()
+    assert np.array_equal(A.indptr, g[f"{case}/indptr"])
+    assert np.array_equal(A.indices, g[f"{case}/indices"])
+    assert A.data.tobytes() == g[f"{case}/data"].tobytes()
+    assert o.rhs.tobytes() == g[f"{case}/Q"].tobytes()
+    assert o.jacobi_diag().tobytes() == g[f"{case}/jac"].tobytes()
+    x = probe_vector(o.R)
+    assert o.apply(x).tobytes() == g[f"{case}/Ax"].tobytes()
+    assert o.apply(x, transpose=True).tobytes() == g[f"{case}/Atx"].tobytes()
+    xs, rep = o.cgnr(tol=1e-9, max_iter=300, blas_threads=FIX_BLAS[0], blas_kernel=FIX_BLAS[1])
+    assert rep["iterations"] == meta["cg0"]["iterations"]
+    assert xs.tobytes() == g[f"{case}/cg0/x"].tobytes()
+    assert np.array(rep["normal_history"]).tobytes() == g[f"{case}/cg0/nh"].tobytes()
+
+
+def test_neumann_redirects_instead_of_dropping():
+    """The reference's own Neumann check (test_solver.py:73-79): redirected
+    writes keep more entries than Dirichlet's dropped ones."""
+    from dataclasses import replace
+    spec = rand_spec(1, (4, 4, 4), 5)
+    nd = StencilOracle(build_tables(1), spec).csr().nnz
+    nn = StencilOracle(build_tables(1), replace(spec, bc="neumann")).csr().nnz
+    assert nn > nd
+
+
+@pytest.mark.reference
+def test_oracle_neumann_matches_live_reference(ref):
+    from dataclasses import replace
+    from pnrte.equations import build_pn
+    from pnrte.solver import assemble
+    from pnrte.stencil import compile_program
+    spec = replace(rand_spec(4, (4, 3, 5), 77), bc="neumann")
+    s = assemble(compile_program(build_pn(4, 3)), spec)
+    A = StencilOracle(build_tables(4), spec).csr()
+    assert np.array_equal(A.indices, s.A.indices) and A.data.tobytes() == s.A.data.tobytes()

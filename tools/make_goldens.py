@@ -7,6 +7,8 @@ Writes
   tables_N{1..7}.json  flattened StencilPrograms of compile_program(build_pn(N,3))
   cases.npz            per small case: reference CSR A, Q, A@x, A.T@x, colsum(A o A),
                        CGNR (plain + Jacobi) x / histories / counts, unstagger(x)
+  neumann.npz/.json    bc="neumann" cases: reference CSR A, Q, A@x, A.T@x, colsum(A o A),
+                       CGNR x / histories (python tools/make_goldens.py --neumann-only)
   configs.json         reference solves of configs 1 and 2: iteration count, sha256
                        of the solution bits, histories, residuals; input hashes
 The numpy/OpenBLAS configuration used is recorded (blas threads and kernel):
@@ -30,7 +32,7 @@ from pnrte.solver import assemble, solve_normal_cg, unstagger  # noqa: E402
 from pnrte.stencil import compile_program  # noqa: E402
 from threadpoolctl import threadpool_info  # noqa: E402
 
-from cases import CASES, CASES_2D, probe_vector, rand_spec  # noqa: E402
+from cases import CASES, CASES_2D, NEUMANN_CASES, case_inputs, probe_vector, rand_spec  # noqa: E402
 from paper_1807_00410_b200.problems import make_checkerboard  # noqa: E402
 from paper_1807_00410_b200.configs import make_config  # noqa: E402
 from paper_1807_00410_b200.program import tables_from_program, to_json  # noqa: E402
@@ -50,7 +52,39 @@ def blas():
     return {}
 
 
+def neumann():
+    arrs = {}
+    meta = {"blas": blas(), "cases": {}}
+    for name in NEUMANN_CASES:
+        _, spec = case_inputs(name)
+        prog = compile_program(build_pn(int(name.split("_")[1][1:]), spec.dim))
+        sysm = assemble(prog, spec)
+        A = sysm.A
+        x = probe_vector(A.shape[0])
+        arrs[f"{name}/indptr"] = A.indptr.astype(np.int64)
+        arrs[f"{name}/indices"] = A.indices.astype(np.int32)
+        arrs[f"{name}/data"] = A.data
+        arrs[f"{name}/Q"] = sysm.Q
+        arrs[f"{name}/Ax"] = A @ x
+        arrs[f"{name}/Atx"] = A.T @ x
+        arrs[f"{name}/jac"] = np.asarray(A.multiply(A).sum(axis=0)).ravel()
+        xs, rep = solve_normal_cg(sysm, tol=1e-9, max_iter=300)
+        arrs[f"{name}/cg0/x"] = xs
+        arrs[f"{name}/cg0/nh"] = np.array(rep.normal_history)
+        arrs[f"{name}/cg0/ph"] = np.array(rep.primal_history)
+        meta["cases"][name] = {"cg0": {"iterations": rep.iterations, "converged": rep.converged,
+                                       "normal_residual": rep.normal_residual,
+                                       "primal_residual": rep.primal_residual}}
+        print(name, meta["cases"][name], flush=True)
+    np.savez_compressed(GOLD / "neumann.npz", **arrs)
+    (GOLD / "neumann.json").write_text(json.dumps(meta, indent=1))
+
+
 def main():
+    if "--neumann-only" in sys.argv:
+        neumann()
+        return
+    neumann()
     GOLD.mkdir(parents=True, exist_ok=True)
     for N in range(1, 8):
         t = tables_from_program(compile_program(build_pn(N, 3)))
