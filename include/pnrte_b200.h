@@ -88,6 +88,35 @@ const char *pn_last_error(void);
  * buffer of R doubles; Neumann rows are not pinned). */
 int pn_assemble_csr(pn_context *ctx, int32_t bc, double *rhs, pn_context **out, void *stream);
 
+/* General stencil program (coefficients that depend on fields, e.g. the CDA
+ * system of equations.py:213-237): every entry coefficient, diagonal and
+ * residual is a postfix program (paper_1807_00410_b200/general.py) that
+ * pn_assemble_general evaluates per voxel on the device with numpy's
+ * arithmetic, then assembles the CSR exactly as pn_assemble_csr does
+ * (bc 0 Dirichlet / 1 Neumann).  All arrays are HOST arrays except the field
+ * data (DEVICE, the reference's [i,j,k] C-order grids; 2-D: nz = 1).  Ops are
+ * (opcode, argument) pairs: 0 end, 1 push consts[a], 2 push sample a (field
+ * s_slot[a] at voxel + (s_dx, s_dy, s_dz)[a], clamped to the grid), 3 add,
+ * 4 mul, 5 reciprocal, 6 square, 7 sqrt, 8 ones.  The returned CSR context
+ * keeps the grid and row parities, so pn_unstagger works on it. */
+typedef struct {
+    int32_t U, nx, ny, nz;
+    int32_t device;
+    const int32_t *par;          /* [U] row location parity bits (x | y<<1 | z<<2) */
+    const int32_t *e_ptr;        /* [U+1] */
+    const int32_t *e_tgt, *e_dx, *e_dy, *e_dz, *e_diag, *e_code;   /* per entry, program order */
+    const int32_t *r_code;       /* [U] residual program (RHS = -value) */
+    const int32_t *ops; int32_t n_ops;          /* n_ops pairs */
+    const double *consts; int32_t n_consts;
+    const int32_t *s_slot, *s_dx, *s_dy, *s_dz; int32_t n_samples;
+    int32_t n_fields;            /* <= 32 */
+    const int32_t *f_kind;       /* 0 absent (zero), 1 uniform scalar, 2 device array */
+    const double *f_scalar;
+    const double *const *f_data;
+} pn_general_desc;
+
+int pn_assemble_general(const pn_general_desc *desc, int32_t bc, double *rhs, pn_context **out, void *stream);
+
 /* Download a CSR context's A in scipy layout into HOST buffers (the
  * assembled system's A.indptr / A.indices / A.data).  NULL arrays: only
  * *nnz is written. */
@@ -143,6 +172,11 @@ int pn_solve(pn_context *ctx, const pn_solve_opts *opts, const double *b, const 
  * Reads the k-1 plane of z-staggered comps from the lower neighbour on
  * multi-GPU.  out: [nx][ny][nz_local][U]. */
 int pn_unstagger(pn_context *ctx, const double *u, double *out, void *stream);
+
+/* Context-free unstagger for any program (row parities par[U], host):
+ * u and out are device buffers as in pn_unstagger (single GPU). */
+int pn_unstagger_grid(const int32_t *par, int32_t U, int32_t nx, int32_t ny, int32_t nz, const double *u,
+                      double *out, void *stream);
 
 /* Host-buffer composite (e2e): host fields already set, host x out. */
 int pn_solve_host(pn_context *ctx, const pn_solve_opts *opts, double *x_host,

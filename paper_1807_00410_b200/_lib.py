@@ -44,6 +44,15 @@ class Desc(ctypes.Structure):
                 ("nccl_id", P), ("rank", I32), ("world", I32)]
 
 
+class GeneralDesc(ctypes.Structure):
+    """pn_general_desc (include/pnrte_b200.h)."""
+    _fields_ = [(n, I32) for n in ("U", "nx", "ny", "nz", "device")] + \
+        [(n, P) for n in ("par", "e_ptr", "e_tgt", "e_dx", "e_dy", "e_dz", "e_diag", "e_code", "r_code", "ops")] + \
+        [("n_ops", I32), ("consts", P), ("n_consts", I32)] + \
+        [(n, P) for n in ("s_slot", "s_dx", "s_dy", "s_dz")] + [("n_samples", I32), ("n_fields", I32)] + \
+        [(n, P) for n in ("f_kind", "f_scalar", "f_data")]
+
+
 class SolveOpts(ctypes.Structure):
     _fields_ = [("tol", F64), ("max_iter", I64), ("primal_tol", F64), ("jacobi", I32), ("mode", I32),
                 ("blas_threads", I32), ("blas_kernel", I32), ("check_every", I32)]
@@ -75,6 +84,8 @@ def load():
         "pn_destroy": [P],
         "pn_assemble_csr": [P, I32, P, ctypes.POINTER(P), P],
         "pn_csr_export": [P, ctypes.POINTER(I64), P, P, P],
+        "pn_assemble_general": [ctypes.POINTER(GeneralDesc), I32, P, ctypes.POINTER(P), P],
+        "pn_unstagger_grid": [P, I32, I32, I32, I32, P, P, P],
         "pn_set_field": [P, I32, I32, F64, P, P],
         "pn_setup": [P, P],
         "pn_export_diag_rhs": [P, P, P, P],

@@ -248,9 +248,142 @@ int stencil_csr_assemble(pn_context *c, int neumann, cudaStream_t s, long long *
     return st;
 }
 
+// ---------------------------------------------------------------------------
+// General programs (field-dependent coefficients, e.g. CDA): every entry,
+// diagonal and residual is a postfix program (general.py) evaluated per
+// voxel with the reference's numpy arithmetic -- one IEEE op per array
+// operation (this file is built with -fmad=false), reciprocal for ** -1.
+// st: caller-owned evaluation stack (GEN_STACK doubles).  It is declared in
+// the kernel on purpose: as a local of this (inlined) function NVVM's stack
+// colouring placed it on top of the caller's live val[] array.
+__device__ double gen_eval(const GenProg &P, int pc, int i, int j, int k, double *st) {
+    int sp = 0;
+    for (;; ++pc) {
+        const int op = P.ops[2 * pc], arg = P.ops[2 * pc + 1];
+        switch (op) {
+        case G_END: return st[0];
+        case G_NUM: st[sp++] = P.consts[arg]; break;
+        case G_FIELD: {
+            const int f = P.s_slot[arg];
+            double v = 0.0;
+            if (P.f_kind[f] == 1) v = P.f_scalar[f];
+            else if (P.f_kind[f] == 2) {
+                const int ii = min(max(i + P.s_dx[arg], 0), P.nx - 1);
+                const int jj = min(max(j + P.s_dy[arg], 0), P.ny - 1);
+                const int kk = min(max(k + P.s_dz[arg], 0), P.nz - 1);
+                v = P.f_data[f][((long long)ii * P.ny + jj) * P.nz + kk];
+            }
+            st[sp++] = v;
+            break;
+        }
+        case G_ADD: --sp; st[sp - 1] = __dadd_rn(st[sp - 1], st[sp]); break;
+        case G_MUL: --sp; st[sp - 1] = __dmul_rn(st[sp - 1], st[sp]); break;
+        case G_RECIP: st[sp - 1] = __ddiv_rn(1.0, st[sp - 1]); break;
+        case G_SQUARE: st[sp - 1] = __dmul_rn(st[sp - 1], st[sp - 1]); break;
+        case G_SQRT: st[sp - 1] = __dsqrt_rn(st[sp - 1]); break;
+        case G_ONE: st[sp - 1] = 1.0; break;
+        default: return __longlong_as_double(0x7ff8000000000000LL);
+        }
+    }
+}
+
+// one thread per row (v, c): entries in program order -> masked (Dirichlet,
+// solver.py:151-163) or clipped (Neumann, :146-147) columns, insertion-sorted
+// and duplicate-summed as in k_stencil_csr; RHS = -(residual), pinned rows 0
+__global__ void k_general_csr(GenProg P, int neumann, long long *cnt, const long long *__restrict__ ap, int *aj,
+                              double *ax, double *rhs) {
+    const long long pvox = (long long)P.nx * P.ny;
+    const long long row = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (row >= pvox * P.nz * P.U) return;
+    const long long v = row / P.U;
+    const int c = (int)(row - v * P.U);
+    const int i = (int)(v % P.nx), j = (int)((v / P.nx) % P.ny), k = (int)(v / pvox);
+    const int bb = (i == P.nx - 1) | ((j == P.ny - 1) << 1) | ((k == P.nz - 1) << 2);
+    const bool pinned = !neumann && (P.par[c] & bb);
+    double st[GEN_STACK];
+    if (rhs) {
+        const double r = -gen_eval(P, P.r_code[c], i, j, k, st);
+        rhs[row] = pinned ? 0.0 : r;
+        return;
+    }
+    int col[ASM_MAX];
+    double val[ASM_MAX];
+    int n = 0;
+    for (int e = P.e_ptr[c]; e < P.e_ptr[c + 1]; ++e) {
+        const int o = P.e_tgt[e];
+        int ii = i + P.e_dx[e], jj = j + P.e_dy[e], kk = k + P.e_dz[e];
+        const bool in = ii >= 0 && jj >= 0 && kk >= 0 && ii < P.nx && jj < P.ny && kk < P.nz;
+        if (!neumann) {
+            if (!in) continue;
+            if (!P.e_diag[e]) {
+                const int nbb = (ii == P.nx - 1) | ((jj == P.ny - 1) << 1) | ((kk == P.nz - 1) << 2);
+                if (pinned || (P.par[o] & nbb)) continue;
+            }
+        }
+        ii = min(max(ii, 0), P.nx - 1);
+        jj = min(max(jj, 0), P.ny - 1);
+        kk = min(max(kk, 0), P.nz - 1);
+        const int cc = (int)(((long long)kk * pvox + (long long)jj * P.nx + ii) * P.U + o);
+        const double a = gen_eval(P, P.e_code[e], i, j, k, st);
+        int p = n;
+        while (p > 0 && col[p - 1] > cc) --p;
+        if (p > 0 && col[p - 1] == cc) {
+            val[p - 1] = __dadd_rn(val[p - 1], a);
+            continue;
+        }
+        for (int q = n; q > p; --q) { col[q] = col[q - 1]; val[q] = val[q - 1]; }
+        col[p] = cc;
+        val[p] = a;
+        ++n;
+    }
+    if (!ap) {
+        cnt[row] = n;
+        return;
+    }
+    const long long base = ap[row];
+    for (int q = 0; q < n; ++q) { aj[base + q] = col[q]; ax[base + q] = val[q]; }
+}
+
+int general_csr_assemble(const GenProg &P, int neumann, double *rhs, cudaStream_t s, long long **ap_out,
+                         int **aj_out, double **ax_out, long long *nnz_out) {
+    const long long R = (long long)P.nx * P.ny * P.nz * P.U;
+    long long *cnt = nullptr, *ap = nullptr;
+    int *aj = nullptr;
+    double *ax = nullptr;
+    void *tmp = nullptr;
+    size_t tmp_bytes = 0;
+    long long nnz = 0;
+    const unsigned nb = (unsigned)((R + 127) / 128);
+    auto fail = [&](int code) { cudaFree(cnt); cudaFree(ap); cudaFree(aj); cudaFree(ax); cudaFree(tmp); return code; };
+    if (rhs) {
+        k_general_csr<<<nb, 128, 0, s>>>(P, neumann, nullptr, nullptr, nullptr, nullptr, rhs);
+        if (cudaGetLastError() != cudaSuccess) return fail(PN_ERR_CUDA);
+    }
+    if (cudaMalloc(&cnt, (R + 1) * 8) != cudaSuccess || cudaMalloc(&ap, (R + 1) * 8) != cudaSuccess)
+        return fail(PN_ERR_NOMEM);
+    if (cudaMemsetAsync(cnt, 0, (R + 1) * 8, s) != cudaSuccess) return fail(PN_ERR_CUDA);
+    k_general_csr<<<nb, 128, 0, s>>>(P, neumann, cnt, nullptr, nullptr, nullptr, nullptr);
+    if (cudaGetLastError() != cudaSuccess) return fail(PN_ERR_CUDA);
+    cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, cnt, ap, (int)(R + 1), s);
+    if (cudaMalloc(&tmp, std::max<size_t>(tmp_bytes, 1)) != cudaSuccess) return fail(PN_ERR_NOMEM);
+    if (cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt, ap, (int)(R + 1), s) != cudaSuccess) return fail(PN_ERR_CUDA);
+    if (cudaMemcpyAsync(&nnz, ap + R, 8, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess)
+        return fail(PN_ERR_CUDA);
+    if (cudaMalloc(&aj, std::max<long long>(nnz, 1) * sizeof(int)) != cudaSuccess ||
+        cudaMalloc(&ax, std::max<long long>(nnz, 1) * sizeof(double)) != cudaSuccess)
+        return fail(PN_ERR_NOMEM);
+    k_general_csr<<<nb, 128, 0, s>>>(P, neumann, nullptr, ap, aj, ax, nullptr);
+    if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(s) != cudaSuccess) return fail(PN_ERR_CUDA);
+    cudaFree(cnt);
+    cudaFree(tmp);
+    *ap_out = ap; *aj_out = aj; *ax_out = ax; *nnz_out = nnz;
+    return PN_OK;
+}
+
 void csr_release(pn_context *c) {
     CsrOp &o = c->csr;
-    for (void *p : {(void *)o.ap, (void *)o.aj, (void *)o.ax, (void *)o.tp, (void *)o.tj, (void *)o.tx})
+    for (void *p : {(void *)o.ap, (void *)o.aj, (void *)o.ax, (void *)o.tp, (void *)o.tj, (void *)o.tx, (void *)o.upar})
         if (p) cudaFree(p);
     o = CsrOp{};
 }

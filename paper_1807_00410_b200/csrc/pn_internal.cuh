@@ -76,6 +76,24 @@ struct CsrOp {
     long long *ap = nullptr, *tp = nullptr;
     int *aj = nullptr, *tj = nullptr;
     double *ax = nullptr, *tx = nullptr;
+    // grid of the stencil program the system was assembled from (unstagger)
+    int *upar = nullptr;
+    Geo ug{};
+};
+
+// general stencil program (pn_csr.cu, pn_assemble_general): postfix
+// coefficient programs over field samples, device copies of pn_general_desc
+enum GenOp { G_END = 0, G_NUM, G_FIELD, G_ADD, G_MUL, G_RECIP, G_SQUARE, G_SQRT, G_ONE };
+constexpr int GEN_STACK = 16;
+constexpr int GEN_FIELDS = 32;
+struct GenProg {
+    int U, nx, ny, nz;
+    const int *par, *e_ptr, *e_tgt, *e_dx, *e_dy, *e_dz, *e_diag, *e_code, *r_code, *ops;
+    const double *consts;
+    const int *s_slot, *s_dx, *s_dy, *s_dz;
+    int f_kind[GEN_FIELDS];
+    double f_scalar[GEN_FIELDS];
+    const double *f_data[GEN_FIELDS];   // reference [i][j][k] C-order arrays
 };
 
 // ------------------------------------------------------------- context --
@@ -184,6 +202,8 @@ int csr_build(pn_context *c, long long n, long long nnz, const long long *ap, co
 constexpr int ASM_MAX = 48;
 int stencil_csr_assemble(pn_context *c, int neumann, cudaStream_t s, long long **ap, int **aj, double **ax,
                          long long *nnz);
+int general_csr_assemble(const GenProg &P, int neumann, double *rhs, cudaStream_t s, long long **ap, int **aj,
+                         double **ax, long long *nnz);
 void csr_release(pn_context *c);
 int launch_csr_apply(pn_context *c, int trans, int faithful, int squared, const double *x, double *y, int red,
                      const double *minv, double *zt, cudaStream_t s, bool gated);

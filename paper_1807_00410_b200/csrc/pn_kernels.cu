@@ -668,8 +668,11 @@ __global__ void k_unstagger(const int *__restrict__ par, Geo g, const double *__
 }
 
 int launch_unstagger(pn_context *c, const double *u, double *out, cudaStream_t s) {
-    long long total = (long long)c->g.nx * c->g.ny * c->g.nzl * c->U;
-    k_unstagger<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(c->tb.par, c->g, u, out);
+    // CSR systems assembled from a stencil program keep its grid and parities
+    const Geo &g = c->is_csr ? c->csr.ug : c->g;
+    const int *par = c->is_csr ? c->csr.upar : c->tb.par;
+    long long total = (long long)g.nx * g.ny * g.nzl * g.U;
+    k_unstagger<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(par, g, u, out);
     PN_CUDA(cudaGetLastError());
     c->launches++;
     return PN_OK;

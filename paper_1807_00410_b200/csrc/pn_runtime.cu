@@ -312,6 +312,118 @@ int pn_assemble_csr(pn_context *c, int32_t bc, double *rhs, pn_context **out, vo
     PN_TRY(stencil_csr_assemble(c, bc, s, &ap, &aj, &ax, &nnz));
     int st = create_csr_ctx(R, nnz, (const int64_t *)ap, aj, ax, c->device, out);
     cudaFree(ap); cudaFree(aj); cudaFree(ax);
+    if (st == PN_OK) {
+        pn_context *o = *out;
+        o->csr.ug = c->g;
+        if (cudaMalloc(&o->csr.upar, c->U * sizeof(int)) != cudaSuccess ||
+            cudaMemcpy(o->csr.upar, c->tb.par, c->U * sizeof(int), cudaMemcpyDeviceToDevice) != cudaSuccess) {
+            pn_destroy(o);
+            *out = nullptr;
+            set_error("out of device memory");
+            return PN_ERR_NOMEM;
+        }
+    }
+    return st;
+}
+
+int pn_assemble_general(const pn_general_desc *d, int32_t bc, double *rhs, pn_context **out, void *stream) {
+    if (!d || !out || (bc != 0 && bc != 1) || d->U < 1 || d->nx < 1 || d->ny < 1 || d->nz < 1 || !d->par ||
+        !d->e_ptr || !d->r_code || !d->ops || d->n_ops < 1 || d->n_fields < 0 || d->n_fields > GEN_FIELDS) {
+        set_error("invalid general program");
+        return PN_ERR_INVALID;
+    }
+    const long long R = (long long)d->nx * d->ny * d->nz * d->U;
+    if (R >= (1LL << 31)) { set_error("system too large for 32-bit CSR indices"); return PN_ERR_UNSUPPORTED; }
+    const int U = d->U, ne = d->e_ptr[U];
+    for (int c = 0; c < U; ++c)
+        if (d->e_ptr[c + 1] - d->e_ptr[c] > ASM_MAX || d->e_ptr[c + 1] < d->e_ptr[c]) {
+            set_error("stencil row too long for CSR assembly");
+            return PN_ERR_UNSUPPORTED;
+        }
+    // validate every program: operands in range, stack within GEN_STACK, one value left
+    auto check_prog = [&](int pc) {
+        int sp = 0;
+        for (; pc >= 0 && pc < d->n_ops; ++pc) {
+            const int op = d->ops[2 * pc], a = d->ops[2 * pc + 1];
+            if (op == G_END) return sp == 1;
+            if (op == G_NUM) { if (a < 0 || a >= d->n_consts) return false; ++sp; }
+            else if (op == G_FIELD) {
+                if (a < 0 || a >= d->n_samples || d->s_slot[a] < 0 || d->s_slot[a] >= d->n_fields) return false;
+                ++sp;
+            } else if (op == G_ADD || op == G_MUL) { if (sp < 2) return false; --sp; }
+            else if (op >= G_RECIP && op <= G_ONE) { if (sp < 1) return false; }
+            else return false;
+            if (sp > GEN_STACK) return false;
+        }
+        return false;
+    };
+    for (int e = 0; e < ne; ++e)
+        if (d->e_tgt[e] < 0 || d->e_tgt[e] >= U || !check_prog(d->e_code[e])) {
+            set_error("malformed coefficient program");
+            return PN_ERR_INVALID;
+        }
+    for (int c = 0; c < U; ++c)
+        if (!check_prog(d->r_code[c])) { set_error("malformed residual program"); return PN_ERR_INVALID; }
+    PN_CUDA(cudaSetDevice(d->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    GenProg P{};
+    P.U = U; P.nx = d->nx; P.ny = d->ny; P.nz = d->nz;
+    std::vector<void *> owned;
+    bool ok = true;
+    auto up = [&](const void *src, size_t bytes) -> void * {
+        void *p = nullptr;
+        if (cudaMalloc(&p, std::max<size_t>(bytes, 8)) != cudaSuccess) { ok = false; return nullptr; }
+        owned.push_back(p);
+        if (bytes && cudaMemcpy(p, src, bytes, cudaMemcpyHostToDevice) != cudaSuccess) ok = false;
+        return p;
+    };
+    const size_t I = sizeof(int);
+    P.par = (const int *)up(d->par, U * I);
+    P.e_ptr = (const int *)up(d->e_ptr, (U + 1) * I);
+    P.e_tgt = (const int *)up(d->e_tgt, ne * I);
+    P.e_dx = (const int *)up(d->e_dx, ne * I);
+    P.e_dy = (const int *)up(d->e_dy, ne * I);
+    P.e_dz = (const int *)up(d->e_dz, ne * I);
+    P.e_diag = (const int *)up(d->e_diag, ne * I);
+    P.e_code = (const int *)up(d->e_code, ne * I);
+    P.r_code = (const int *)up(d->r_code, U * I);
+    P.ops = (const int *)up(d->ops, 2 * (size_t)d->n_ops * I);
+    P.consts = (const double *)up(d->consts, (size_t)d->n_consts * sizeof(double));
+    P.s_slot = (const int *)up(d->s_slot, (size_t)d->n_samples * I);
+    P.s_dx = (const int *)up(d->s_dx, (size_t)d->n_samples * I);
+    P.s_dy = (const int *)up(d->s_dy, (size_t)d->n_samples * I);
+    P.s_dz = (const int *)up(d->s_dz, (size_t)d->n_samples * I);
+    for (int f = 0; f < d->n_fields; ++f) {
+        P.f_kind[f] = d->f_kind[f];
+        P.f_scalar[f] = d->f_scalar[f];
+        P.f_data[f] = d->f_kind[f] == 2 ? d->f_data[f] : nullptr;
+        if (d->f_kind[f] == 2 && !d->f_data[f]) { P.f_kind[f] = -1; }
+    }
+    auto release = [&]() { for (void *p : owned) cudaFree(p); };
+    for (int f = 0; f < d->n_fields; ++f)
+        if (P.f_kind[f] < 0 || P.f_kind[f] > 2) { release(); set_error("invalid field slot"); return PN_ERR_INVALID; }
+    if (!ok) { release(); set_error("out of device memory"); return PN_ERR_NOMEM; }
+    long long *ap;
+    int *aj;
+    double *ax;
+    long long nnz;
+    int st = general_csr_assemble(P, bc, rhs, s, &ap, &aj, &ax, &nnz);
+    if (st == PN_OK) {
+        st = create_csr_ctx(R, nnz, (const int64_t *)ap, aj, ax, d->device, out);
+        cudaFree(ap); cudaFree(aj); cudaFree(ax);
+    }
+    if (st == PN_OK) {
+        pn_context *o = *out;
+        Geo &g = o->csr.ug;
+        g.U = U; g.nx = d->nx; g.ny = d->ny; g.nz = d->nz; g.z0 = 0; g.nzl = d->nz;
+        g.pvox = (long long)d->nx * d->ny;
+        g.plane = g.pvox * U;
+        o->csr.upar = (int *)P.par;   // ownership moves to the CSR context
+        owned.erase(std::find(owned.begin(), owned.end(), (void *)P.par));
+    } else {
+        set_error("general CSR assembly failed");
+    }
+    release();
     return st;
 }
 
@@ -776,13 +888,36 @@ int pn_group_solve(pn_context **ctxs, int32_t n, const pn_solve_opts *o, double 
 }
 
 int pn_unstagger(pn_context *c, const double *u, double *out, void *stream) {
-    if (c && c->is_csr) { set_error("not available for a generic CSR system"); return PN_ERR_UNSUPPORTED; }
+    if (c && c->is_csr) {
+        if (!c->csr.upar) { set_error("not available for a generic CSR system"); return PN_ERR_UNSUPPORTED; }
+        return launch_unstagger(c, u, out, (cudaStream_t)stream);
+    }
     cudaStream_t s = (cudaStream_t)stream;
     PN_TRY(alloc_buf(c, c->tmp));
     PN_CUDA(cudaMemcpyAsync(c->tmp.p, u, c->R_l() * sizeof(double), cudaMemcpyDeviceToDevice, s));
     std::vector<pn_context *> cs{c};
     PN_TRY(halo_exchange(cs, &pn_context::tmp, s));
     return launch_unstagger(c, c->tmp.p, out, s);
+}
+
+int pn_unstagger_grid(const int32_t *par, int32_t U, int32_t nx, int32_t ny, int32_t nz, const double *u,
+                      double *out, void *stream) {
+    if (!par || U < 1 || nx < 1 || ny < 1 || nz < 1 || !u || !out) { set_error("invalid arguments"); return PN_ERR_INVALID; }
+    pn_context c;
+    c.is_csr = true;
+    Geo &g = c.csr.ug;
+    g.U = U; g.nx = nx; g.ny = ny; g.nz = nz; g.z0 = 0; g.nzl = nz;
+    g.pvox = (long long)nx * ny;
+    g.plane = g.pvox * U;
+    PN_CUDA(cudaMalloc(&c.csr.upar, U * sizeof(int)));
+    cudaStream_t s = (cudaStream_t)stream;
+    int st = PN_OK;
+    if (cudaMemcpyAsync(c.csr.upar, par, U * sizeof(int), cudaMemcpyHostToDevice, s) != cudaSuccess) st = PN_ERR_CUDA;
+    if (st == PN_OK) st = launch_unstagger(&c, u, out, s);
+    cudaStreamSynchronize(s);
+    cudaFree(c.csr.upar);
+    c.csr.upar = nullptr;
+    return st;
 }
 
 int pn_solve_host(pn_context *c, const pn_solve_opts *o, double *x_host, pn_report *rep, double *hn, double *hp,

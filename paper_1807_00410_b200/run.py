@@ -11,8 +11,10 @@ internal error.
 
 Problems: `pointsource` (homogeneous medium, unit point emitter,
 problems.py:130-156 restated) and the BASELINE configurations `cfg1`..`cfg5`
-(configs.py).  The 2-D checkerboard and the CDA method are outside the
-matrix-free 3-D P_N path and are rejected as config errors.
+(configs.py).  Methods: `pn` (matrix-free P_N stencil) and `cda` (collapsed
+diffusion, field-dependent couplings: explicit device CSR from
+general.py, field order 0 as cli.py:156).  The 2-D checkerboard is not a
+`run` problem here.
 """
 
 from __future__ import annotations
@@ -41,7 +43,7 @@ class ConfigError(Exception):
 @dataclass
 class RunConfig:
     problem: str = "pointsource"
-    method: str = "pn"
+    method: str = "pn"            # pn | cda
     order: int = 1
     res: int = 0                  # 0 = problem default
     floor: float = -1.0           # < 0 = problem default
@@ -57,9 +59,9 @@ class RunConfig:
     def validated(self):
         if self.problem not in PROBLEMS:
             raise ConfigError(f"unknown problem {self.problem!r}")
-        if self.method != "pn":
-            raise ConfigError(f"method {self.method!r} is outside the matrix-free P_N path")
-        if self.order < 1:
+        if self.method not in ("pn", "cda"):
+            raise ConfigError(f"unknown method {self.method!r}")
+        if self.method == "pn" and self.order < 1:
             raise ConfigError(f"order must be >= 1, got {self.order}")
         if self.tol <= 0:
             raise ConfigError("tol must be positive")
@@ -152,6 +154,8 @@ def run(cfg, log=print):
     from .solver import PnContext
     spec = build_problem(cfg)
     validate_for_solve(spec)
+    if cfg.method == "cda":
+        return _run_cda(cfg, spec, log)
     tables = build_tables(cfg.order)
     os.makedirs(cfg.out, exist_ok=True)
     ctx = PnContext(tables, spec.res, spec.h, device=cfg.device)
@@ -164,15 +168,33 @@ def run(cfg, log=print):
         op, b = ctx, None
         log(f"assembled {R} rows on cuda:{cfg.device} (matrix-free P{cfg.order} stencil)")
     x, report = op.solve(tol=cfg.tol, max_iter=cfg.max_iter, jacobi=cfg.jacobi, mode=cfg.mode, b=b)
+    coll = ctx.unstagger(x).cpu().numpy()
+    _write(cfg, spec, R, coll, cfg.order, report, log)
+    return report
+
+
+def _run_cda(cfg, spec, log):
+    from .general import build_cda_program
+    from .solver import assemble_general
+    os.makedirs(cfg.out, exist_ok=True)
+    csr, q = assemble_general(build_cda_program(spec.dim), spec, device=cfg.device)
+    R = csr.R_local
+    log(f"assembled {R} rows on cuda:{cfg.device} (CDA: explicit device CSR, field-dependent couplings)")
+    x, report = csr.solve(tol=cfg.tol, max_iter=cfg.max_iter, jacobi=cfg.jacobi, mode=cfg.mode, b=q)
+    coll = csr.unstagger(x).cpu().numpy()
+    _write(cfg, spec, R, coll, 0, report, log)
+    return report
+
+
+def _write(cfg, spec, R, coll, order, report, log):
     log(f"solve: {report.iterations} iterations, converged={report.converged}, "
         f"normal={report.normal_residual:.3e}, primal={report.primal_residual:.3e}, "
         f"wall={report.wall_time:.2f}s")
-    coll = ctx.unstagger(x).cpu().numpy()
-    fio.write_field(os.path.join(cfg.out, "field.pnfld"), coll, cfg.order)
+    fio.write_field(os.path.join(cfg.out, "field.pnfld"), coll, order)
     r, line = center_profile(spec, coll)
     fio.write_profile(os.path.join(cfg.out, "profile.csv"), zip(r, line))
     with open(os.path.join(cfg.out, "solve.log"), "w") as fh:
-        fh.write(f"rows {R}\nmode {cfg.mode}\nbc {spec.bc}\n")
+        fh.write(f"rows {R}\nmethod {cfg.method}\nmode {cfg.mode}\nbc {spec.bc}\n")
         fh.write(f"iterations {report.iterations}\nconverged {report.converged}\n")
         fh.write(f"normal_residual {report.normal_residual!r}\nprimal_residual {report.primal_residual!r}\n")
         fh.write(f"wall_time {report.wall_time!r}\n# iter normal primal\n")

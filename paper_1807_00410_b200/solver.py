@@ -186,7 +186,15 @@ class PnContext:
                                                ctypes.byref(handle), _stream(torch)))
         csr = PnContext._csr_shell(self.R_local, self.device)
         csr.handle = handle
+        csr._grid(self.res, self.U, self.dim)
         return csr, q
+
+    def _grid(self, res3, U, dim):
+        """CSR context assembled from a stencil program: keep its grid for unstagger."""
+        self.res = tuple(res3)
+        self.nz_local = self.res[2]
+        self.U = U
+        self.dim = dim
 
     def csr_export(self):
         """A of a CSR context as a scipy matrix (pn_csr_export)."""
@@ -353,6 +361,57 @@ class CsrOperator(StencilOperator):
         return CsrOperator(self.ctx, not self.transpose)
 
 
+def _res3(res):
+    res = tuple(int(r) for r in res)
+    return res + (1,) * (3 - len(res))
+
+
+def assemble_general(program, spec, device=0):
+    """Explicit device CSR of a general stencil program (field-dependent
+    coefficients, e.g. CDA): pn_assemble_general evaluates the compiled
+    coefficient programs per voxel (general.py).  Returns (CSR context, Q)."""
+    from .general import compile_general
+    torch = _torch()
+    L = _lib.load()
+    bc = _bc(spec)
+    gt = compile_general(program, spec.h)
+    res3 = _res3(spec.res)
+    R = int(np.prod(res3)) * gt.U
+    dev = torch.device("cuda", int(device))
+    held = []
+    nf = len(gt.field_names)
+    kinds = np.zeros(max(nf, 1), np.int32)
+    scalars = np.zeros(max(nf, 1))
+    ptrs = (ctypes.c_void_p * max(nf, 1))()
+    for f, name in enumerate(gt.field_names):
+        kind, scal, arr = field_slot(spec, name)
+        kinds[f], scalars[f] = kind, scal
+        if kind == 2:
+            t = torch.from_numpy(np.ascontiguousarray(np.asarray(arr, np.float64).reshape(res3))).to(dev)
+            held.append(t)
+            ptrs[f] = t.data_ptr()
+    d = _lib.GeneralDesc()
+    d.U, (d.nx, d.ny, d.nz), d.device = gt.U, res3, int(device)
+    for name in ("par", "e_ptr", "e_tgt", "e_dx", "e_dy", "e_dz", "e_diag", "e_code", "r_code", "ops", "consts",
+                 "s_slot", "s_dx", "s_dy", "s_dz"):
+        setattr(d, name, getattr(gt, name).ctypes.data_as(ctypes.c_void_p))
+    d.n_ops, d.n_consts, d.n_samples = len(gt.ops) // 2, len(gt.consts), len(gt.s_slot)
+    d.n_fields = nf
+    d.f_kind, d.f_scalar = kinds.ctypes.data_as(ctypes.c_void_p), scalars.ctypes.data_as(ctypes.c_void_p)
+    d.f_data = ctypes.cast(ptrs, ctypes.c_void_p)
+    q = torch.empty(R, dtype=torch.float64, device=dev)
+    handle = ctypes.c_void_p()
+    with torch.cuda.device(int(device)):
+        _lib.check(L.pn_assemble_general(ctypes.byref(d), 1 if bc == "neumann" else 0, ctypes.c_void_p(q.data_ptr()),
+                                         ctypes.byref(handle), _stream(torch)))
+        torch.cuda.current_stream().synchronize()
+    del held
+    csr = PnContext._csr_shell(R, device)
+    csr.handle = handle
+    csr._grid(res3, gt.U, program.dim)
+    return csr, q
+
+
 def _check_dim(program, spec):
     dim = getattr(program, "dim", 3)
     if len(tuple(spec.res)) not in (2, 3):
@@ -373,8 +432,12 @@ def assemble(program, spec, device=0):
     device (solver.py:96-186).  Dirichlet: A is matrix-free.  Neumann: the
     redirected writes are assembled into an explicit device CSR (same
     entries as the reference's coo->csr), A is a CsrOperator over it."""
+    from .general import is_general
     _check_dim(program, spec)
     bc = _bc(spec)
+    if is_general(program):
+        csr, q = assemble_general(program, spec, device=device)
+        return SparseSystem(A=CsrOperator(csr), Q=q.cpu().numpy(), res=tuple(spec.res), n_unknowns=csr.U)
     tables = as_tables(program)
     ctx = PnContext(tables, spec.res, spec.h, device=device)
     ctx.set_fields(spec)
@@ -408,6 +471,20 @@ def solve_normal_cg(system, tol=1e-8, max_iter=50000, primal_tol=None, jacobi=Fa
 
 def unstagger(u, program, res, device=0):
     """Collocated (*res, U) coefficients (solver.py:275-296) on the device."""
+    from .general import compile_general, is_general
+    if is_general(program):
+        torch = _torch()
+        gt = compile_general(program, 1.0)
+        res3 = _res3(res)
+        dev = torch.device("cuda", int(device))
+        ut = torch.as_tensor(np.asarray(u, np.float64), device=dev).contiguous()
+        out = torch.empty(res3 + (gt.U,), dtype=torch.float64, device=dev)
+        with torch.cuda.device(int(device)):
+            _lib.check(_lib.load().pn_unstagger_grid(gt.par.ctypes.data_as(ctypes.c_void_p), gt.U, *res3,
+                                                     ctypes.c_void_p(ut.data_ptr()), ctypes.c_void_p(out.data_ptr()),
+                                                     _stream(torch)))
+        out = out.cpu().numpy()
+        return out[:, :, 0] if len(tuple(res)) == 2 else out
     tables = as_tables(program)
     ctx = PnContext(tables, res, 1.0, device=device)
     return ctx.unstagger(u).cpu().numpy()
@@ -422,6 +499,18 @@ def solve_pn(program_or_N, spec, tol=1e-8, max_iter=50000, primal_tol=None, jaco
              mode="fast", device=0, return_staggered=False, **kw):
     """The north-star entry point: order + fields in, (N+1)^2 collocated SH
     coefficients per voxel out (cli.py:136-155 without file I/O)."""
+    from .general import is_general
+    if is_general(program_or_N):
+        _check_dim(program_or_N, spec)
+        if tol <= 0:
+            raise ValueError("tolerance must be positive")
+        csr, q = assemble_general(program_or_N, spec, device=device)
+        x, rep = csr.solve(tol=tol, max_iter=max_iter, primal_tol=primal_tol, jacobi=jacobi, x0=x0, b=q, mode=mode,
+                           **kw)
+        coll = csr.unstagger(x).cpu().numpy()
+        if return_staggered:
+            return coll, rep, x.cpu().numpy()
+        return coll, rep
     tables = as_tables(program_or_N)
     _check_dim(tables, spec)
     bc = _bc(spec)

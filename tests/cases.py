@@ -52,6 +52,31 @@ CASES_NEUMANN_2D = [("ncb_p2_15", 2, 15), ("ncb_p3_21", 3, 21)]
 NEUMANN_CASES = [c[0] for c in CASES_NEUMANN] + [c[0] for c in CASES_NEUMANN_2D]
 
 
+# CDA (collapsed diffusion, equations.py:213-237): field-dependent couplings,
+# served by the general-program device assembly.  (name, dim, res or n, seed, bc)
+CASES_CDA = [
+    ("cda3_654", 3, (6, 5, 4), 51, "dirichlet"),
+    ("cda3_654n", 3, (6, 5, 4), 51, "neumann"),
+    ("cda3_3274", 3, (32, 7, 4), 54, "dirichlet"),
+    ("cda3_111", 3, (1, 1, 1), 53, "dirichlet"),
+    ("cda2_cb15", 2, 15, 0, "dirichlet"),
+    ("cda2_cb15n", 2, 15, 0, "neumann"),
+]
+CDA_CASES = [c[0] for c in CASES_CDA]
+
+
+def cda_inputs(name):
+    """(program, spec) of a CDA fixture case (restated program, no reference)."""
+    from dataclasses import replace
+    from paper_1807_00410_b200.general import build_cda_program
+    from paper_1807_00410_b200.problems import make_checkerboard
+    for cname, dim, res, seed, bc in CASES_CDA:
+        if cname == name:
+            spec = rand_spec(1, res, seed) if dim == 3 else make_checkerboard(res)
+            return build_cda_program(dim), replace(spec, bc=bc)
+    raise KeyError(name)
+
+
 def tables_2d(N):
     import json
     import pathlib

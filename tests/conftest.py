@@ -45,5 +45,7 @@ def golden():
         "configs": json.loads((g / "configs.json").read_text()),
         "neumann": np.load(g / "neumann.npz"),
         "neumann_meta": json.loads((g / "neumann.json").read_text()),
+        "cda": np.load(g / "cda.npz"),
+        "cda_meta": json.loads((g / "cda.json").read_text()),
         "dir": g,
     }

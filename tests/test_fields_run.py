@@ -53,7 +53,7 @@ def test_profile_and_config_files(tmp_path):
     assert cfg.problem == "cfg2" and cfg.order == 3 and cfg.jacobi is True
 
 
-@pytest.mark.parametrize("mapping", [{"problem": "checkerboard"}, {"method": "cda"}, {"order": 0},
+@pytest.mark.parametrize("mapping", [{"problem": "checkerboard"}, {"method": "sn"}, {"order": 0},
                                      {"tol": 0}, {"bogus": 1}, {"jacobi": "maybe"}, {"mode": "turbo"},
                                      {"bc": "periodic"}])
 def test_config_errors(mapping):

@@ -9,6 +9,8 @@ Writes
                        CGNR (plain + Jacobi) x / histories / counts, unstagger(x)
   neumann.npz/.json    bc="neumann" cases: reference CSR A, Q, A@x, A.T@x, colsum(A o A),
                        CGNR x / histories (python tools/make_goldens.py --neumann-only)
+  cda.npz/.json        CDA programs (build_cda, 2-D and 3-D, both boundary conditions): reference
+                       CSR A, Q, CGNR x / histories, unstagger (python tools/make_goldens.py --cda-only)
   configs.json         reference solves of configs 1 and 2: iteration count, sha256
                        of the solution bits, histories, residuals; input hashes
 The numpy/OpenBLAS configuration used is recorded (blas threads and kernel):
@@ -32,7 +34,8 @@ from pnrte.solver import assemble, solve_normal_cg, unstagger  # noqa: E402
 from pnrte.stencil import compile_program  # noqa: E402
 from threadpoolctl import threadpool_info  # noqa: E402
 
-from cases import CASES, CASES_2D, NEUMANN_CASES, case_inputs, probe_vector, rand_spec  # noqa: E402
+from cases import (CASES, CASES_2D, CASES_CDA, NEUMANN_CASES, case_inputs, cda_inputs, probe_vector,  # noqa: E402
+                   rand_spec)
 from paper_1807_00410_b200.problems import make_checkerboard  # noqa: E402
 from paper_1807_00410_b200.configs import make_config  # noqa: E402
 from paper_1807_00410_b200.program import tables_from_program, to_json  # noqa: E402
@@ -80,11 +83,43 @@ def neumann():
     (GOLD / "neumann.json").write_text(json.dumps(meta, indent=1))
 
 
+def cda():
+    from pnrte.equations import build_cda
+    arrs = {}
+    meta = {"blas": blas(), "cases": {}}
+    for name, dim, *_ in CASES_CDA:
+        _, spec = cda_inputs(name)
+        prog = compile_program(build_cda(dim))
+        sysm = assemble(prog, spec)
+        A = sysm.A
+        x = probe_vector(A.shape[0])
+        arrs[f"{name}/indptr"] = A.indptr.astype(np.int64)
+        arrs[f"{name}/indices"] = A.indices.astype(np.int32)
+        arrs[f"{name}/data"] = A.data
+        arrs[f"{name}/Q"] = sysm.Q
+        arrs[f"{name}/Ax"] = A @ x
+        arrs[f"{name}/Atx"] = A.T @ x
+        xs, rep = solve_normal_cg(sysm, tol=1e-10, max_iter=500)
+        arrs[f"{name}/cg0/x"] = xs
+        arrs[f"{name}/cg0/nh"] = np.array(rep.normal_history)
+        arrs[f"{name}/cg0/ph"] = np.array(rep.primal_history)
+        arrs[f"{name}/unstagger"] = unstagger(xs, prog, spec.res)
+        meta["cases"][name] = {"cg0": {"iterations": rep.iterations, "converged": rep.converged,
+                                       "normal_residual": rep.normal_residual}}
+        print(name, meta["cases"][name], flush=True)
+    np.savez_compressed(GOLD / "cda.npz", **arrs)
+    (GOLD / "cda.json").write_text(json.dumps(meta, indent=1))
+
+
 def main():
     if "--neumann-only" in sys.argv:
         neumann()
         return
+    if "--cda-only" in sys.argv:
+        cda()
+        return
     neumann()
+    cda()
     GOLD.mkdir(parents=True, exist_ok=True)
     for N in range(1, 8):
         t = tables_from_program(compile_program(build_pn(N, 3)))
