@@ -178,6 +178,22 @@ int pn_unstagger(pn_context *ctx, const double *u, double *out, void *stream);
 int pn_unstagger_grid(const int32_t *par, int32_t U, int32_t nx, int32_t ny, int32_t nz, const double *u,
                       double *out, void *stream);
 
+/* Post-processing of collocated coefficients (DEVICE arrays; grids are the
+ * (*res, U) C-order output of pn_unstagger):
+ *   pn_fluence      out[v] = sqrt(4 pi) * coll[v, 0]                 solver.py:299-301
+ *   pn_trilinear    out[p, q] = trilinear(coll[..., q], pts[p])      solver.py:304-327
+ *   pn_reconstruct  out[p, d] = radiance at pts[p] in direction dirs[d]
+ *                   (trilinear coefficients . real SH basis)        solver.py:330-343
+ * pts: [npts][dim] world positions inside the domain (the caller checks,
+ * as the reference raises OutOfDomainError); dirs: [ndirs][3], any length;
+ * lm: HOST [U][2] (l, m) per component (unknown_order). */
+int pn_fluence(const double *coll, int64_t nvox, int32_t U, double *out, void *stream);
+int pn_trilinear(const double *coll, int32_t dim, const int32_t *res, int32_t U, const double *origin, double h,
+                 int64_t npts, const double *pts, double *out, void *stream);
+int pn_reconstruct(const double *coll, int32_t dim, const int32_t *res, int32_t U, const int32_t *lm,
+                   const double *origin, double h, int64_t npts, const double *pts, int64_t ndirs,
+                   const double *dirs, double *out, void *stream);
+
 /* Host-buffer composite (e2e): host fields already set, host x out. */
 int pn_solve_host(pn_context *ctx, const pn_solve_opts *opts, double *x_host,
                   pn_report *report, double *normal_hist, double *primal_hist, int64_t hist_cap);

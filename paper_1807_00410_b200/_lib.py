@@ -86,6 +86,9 @@ def load():
         "pn_csr_export": [P, ctypes.POINTER(I64), P, P, P],
         "pn_assemble_general": [ctypes.POINTER(GeneralDesc), I32, P, ctypes.POINTER(P), P],
         "pn_unstagger_grid": [P, I32, I32, I32, I32, P, P, P],
+        "pn_fluence": [P, I64, I32, P, P],
+        "pn_trilinear": [P, I32, P, I32, P, F64, I64, P, P, P],
+        "pn_reconstruct": [P, I32, P, I32, P, P, F64, I64, P, I64, P, P, P],
         "pn_set_field": [P, I32, I32, F64, P, P],
         "pn_setup": [P, P],
         "pn_export_diag_rhs": [P, P, P, P],

@@ -34,7 +34,7 @@ def _nccl_dirs():
 
 
 def sources():
-    units = [CSRC / "pn_kernels.cu", CSRC / "pn_runtime.cu", CSRC / "pn_seg.cu", CSRC / "pn_csr.cu"]
+    units = [CSRC / "pn_kernels.cu", CSRC / "pn_runtime.cu", CSRC / "pn_seg.cu", CSRC / "pn_csr.cu", CSRC / "pn_post.cu"]
     units += sorted((CSRC / "generated").glob("pn_seg_N*.cu"))
     return units
 
@@ -43,7 +43,7 @@ def _flags(src, inc):
     f = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-I", str(CSRC), "-I", str(inc), *ARCH]
     f += EXTRA
-    if src.name in ("pn_kernels.cu", "pn_csr.cu"):
+    if src.name in ("pn_kernels.cu", "pn_csr.cu", "pn_post.cu"):
         f.append("-fmad=false")
     return f
 

@@ -490,9 +490,119 @@ def unstagger(u, program, res, device=0):
     return ctx.unstagger(u).cpu().numpy()
 
 
-def fluence(collocated):
-    """sqrt(4 pi) * L00 (solver.py:299-301)."""
-    return SQRT_4PI * collocated[..., 0]
+# ---------------------------------------------------------------------------
+# post-processing on the device (solver.py:264-343).
+# Inputs may be numpy arrays (uploaded, result returned as numpy) or CUDA
+# tensors (result stays on the device).
+# ---------------------------------------------------------------------------
+
+class OutOfDomainError(ValueError):
+    """Reconstruction point outside the domain (solver.py:30-31)."""
+
+
+def unknown_order(program):
+    """(l, m) per solution-vector component, in component order (solver.py:264-266)."""
+    if hasattr(program, "unknown_index"):
+        return sorted(program.unknown_index, key=program.unknown_index.get)
+    return [tuple(lm) for lm in as_tables(program).lm]
+
+
+def component_grid(u, system_res, n_unknowns, comp):
+    """One staggered component as a grid (solver.py:269-272): a strided view."""
+    nvox = int(np.prod(system_res))
+    return u.reshape(nvox, n_unknowns)[:, comp].reshape(system_res, order="F")
+
+
+def _on_device(a, device):
+    torch = _torch()
+    if torch.is_tensor(a):
+        return a.to(dtype=torch.float64).contiguous(), False
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(torch.device("cuda", int(device))), True
+
+
+def fluence(collocated, device=0):
+    """sqrt(4 pi) * L00 (solver.py:299-301), on the device."""
+    torch = _torch()
+    t, host = _on_device(collocated, device)
+    U = int(t.shape[-1])
+    out = torch.empty(t.shape[:-1], dtype=torch.float64, device=t.device)
+    with torch.cuda.device(t.device):
+        _lib.check(_lib.load().pn_fluence(ctypes.c_void_p(t.data_ptr()), out.numel(), U,
+                                          ctypes.c_void_p(out.data_ptr()), _stream(torch)))
+    return out.cpu().numpy() if host else out
+
+
+def _grid_args(spec, shape):
+    dim = int(spec.dim)
+    res = np.ascontiguousarray(spec.res, np.int32)
+    if tuple(shape[:dim]) != tuple(int(r) for r in spec.res):
+        raise ValueError(f"grid shape {tuple(shape)} does not match the spec resolution {tuple(spec.res)}")
+    origin = np.ascontiguousarray(spec.origin, np.float64)
+    return dim, res, origin
+
+
+def _points(x, dim, device):
+    xa = np.asarray(x, dtype=np.float64)
+    single = xa.ndim == 1
+    xa = np.ascontiguousarray(xa.reshape(-1, dim))
+    return xa, single
+
+
+def trilinear(collocated_comp, spec, x, device=0):
+    """Clamped trilinear interpolation of a voxel-centre grid at world
+    position(s) x (solver.py:304-327), bit-identical to the reference's
+    scalar arithmetic.  x: (dim,) -> float, (P, dim) -> (P,) array."""
+    torch = _torch()
+    g, host = _on_device(collocated_comp, device)
+    dim, res, origin = _grid_args(spec, tuple(g.shape))
+    xa, single = _points(x, dim, device)
+    pts = torch.from_numpy(xa).to(g.device)
+    out = torch.empty(len(xa), dtype=torch.float64, device=g.device)
+    with torch.cuda.device(g.device):
+        _lib.check(_lib.load().pn_trilinear(ctypes.c_void_p(g.data_ptr()), dim, res.ctypes.data_as(ctypes.c_void_p), 1,
+                                            origin.ctypes.data_as(ctypes.c_void_p), float(spec.h), len(xa),
+                                            ctypes.c_void_p(pts.data_ptr()), ctypes.c_void_p(out.data_ptr()),
+                                            _stream(torch)))
+    if single:
+        return float(out[0].item())
+    return out.cpu().numpy() if host else out
+
+
+def reconstruct_radiance(collocated, unknowns, spec, x, omega, device=0):
+    """Radiance at world position(s) x in direction(s) omega (solver.py:330-343):
+    trilinear interpolation of every SH coefficient, then the real SH basis
+    dot product, for all point x direction pairs in one device pass.
+    x: (dim,) or (P, dim); omega: (3,) or (D, 3).  Single point and direction
+    -> float, otherwise a (P, D) array.  Raises OutOfDomainError like the
+    reference for points outside the domain."""
+    torch = _torch()
+    c, host = _on_device(collocated, device)
+    dim, res, origin = _grid_args(spec, tuple(c.shape))
+    U = int(c.shape[-1])
+    if len(unknowns) != U:
+        raise ValueError("unknowns must list one (l, m) per component")
+    xa, single_x = _points(x, dim, device)
+    lo = np.asarray(spec.origin, np.float64)
+    hi = lo + np.asarray(spec.extent, np.float64)
+    if not np.all((xa >= lo) & (xa <= hi)):
+        bad = xa[~np.all((xa >= lo) & (xa <= hi), axis=1)][0]
+        raise OutOfDomainError(f"position {tuple(bad)} outside the domain")
+    wa = np.asarray(omega, dtype=np.float64)
+    single_w = wa.ndim == 1
+    wa = np.ascontiguousarray(wa.reshape(-1, 3))
+    lm = np.ascontiguousarray(np.asarray(unknowns, np.int32).reshape(U, 2))
+    pts = torch.from_numpy(xa).to(c.device)
+    dirs = torch.from_numpy(wa).to(c.device)
+    out = torch.empty((len(xa), len(wa)), dtype=torch.float64, device=c.device)
+    with torch.cuda.device(c.device):
+        _lib.check(_lib.load().pn_reconstruct(
+            ctypes.c_void_p(c.data_ptr()), dim, res.ctypes.data_as(ctypes.c_void_p), U,
+            lm.ctypes.data_as(ctypes.c_void_p), origin.ctypes.data_as(ctypes.c_void_p), float(spec.h), len(xa),
+            ctypes.c_void_p(pts.data_ptr()), len(wa), ctypes.c_void_p(dirs.data_ptr()),
+            ctypes.c_void_p(out.data_ptr()), _stream(torch)))
+    if single_x and single_w:
+        return float(out[0, 0].item())
+    return out.cpu().numpy() if host else out
 
 
 def solve_pn(program_or_N, spec, tol=1e-8, max_iter=50000, primal_tol=None, jacobi=False, x0=None,
