@@ -167,64 +167,155 @@ __host__ __device__ constexpr size_t seg_smem_per_warp() {
     return sizeof(double) * ((size_t)32 * (N + 1) * (N + 1) + 2 * (N + 1) * (N + 1) + 2 * 4 * 34);
 }
 
+// one row of one CTA row-group ("virtual block" vb of the tiled traversal):
+// CTAs march in z inside y-tiles of g.tyb row blocks, so the z-neighbour rows
+// (k-1, k+1) are still in L2 when read
+struct SegItem {
+    int seg, jb, kl, j, kg;
+    long long rowbase;
+};
+
+template <int N>
+__device__ __forceinline__ SegItem seg_item(const SegGeo &g, long long vb, int rw) {
+    constexpr long long rowlen = (long long)(N + 1) * (N + 1) * 32;
+    SegItem it;
+    it.seg = (int)(vb % g.nseg);
+    vb /= g.nseg;
+    const int tyb = min(g.tyb, g.nyb);
+    const int jb_in = (int)(vb % tyb);
+    vb /= tyb;
+    it.kl = g.kl0 + (int)(vb % g.npl) * g.kst;
+    it.jb = (int)(vb / g.npl) * tyb + jb_in;
+    it.j = it.jb < g.nyb ? it.jb * SegTune<N>::rows + rw : g.ny;
+    it.kg = g.z0 + it.kl;
+    it.rowbase = (((long long)it.kl * g.ny + it.j) * g.nseg + it.seg) * rowlen;
+    return it;
+}
+
+// issue the row's cp.async copies into buffer xs (split over the warps of
+// the row): the own row (32*U doubles), the four sigma_t / sigma_s rows of
+// the staggered site sets, the x+1 sample of lane 31, and the segment-edge
+// values of the neighbours.  Everything from HBM goes through L2 only.
+template <int N>
+__device__ __forceinline__ void seg_stage(const SegGeo &g, const SegItem &it, double *xs, const double *__restrict__ X,
+                                          const double *__restrict__ st, const double *__restrict__ ss, int lane,
+                                          int half) {
+    constexpr int U = (N + 1) * (N + 1);
+    constexpr int WPR = SegTune<N>::wpr;
+    constexpr long long rowlen = (long long)U * 32;
+    double *ep = xs + 32 * U, *en = ep + U, *sg = en + U;
+    const double *Xrow = X + it.rowbase;
+    const bool has_prev = it.seg > 0, has_next = it.seg < g.nseg - 1;
+#pragma unroll 4
+    for (int q = lane + 32 * half; q < 16 * U; q += 32 * WPR) cp_async16(xs + 2 * q, Xrow + 2 * q);
+    for (int q = lane + 32 * half; q < 128; q += 32 * WPR) {
+        const int rowq = q >> 4, part = (q & 15) * 2, fld = rowq >> 2, r4 = rowq & 3;
+        const int jj = min(it.j + (r4 & 1), g.ny - 1);
+        const int kk = it.kl + (r4 >> 1);   // plane nzl exists (edge-replicated at upload)
+        const long long vb = ((long long)kk * g.ny + jj) * g.nx + it.seg * 32;
+        cp_async16(sg + fld * 136 + r4 * 34 + part, (fld ? ss : st) + vb + part);
+    }
+    if (half == WPR - 1) {
+        if (lane < 8) {   // x+1 sample of lane 31 per sigma row, edge-replicated at nx-1
+            const int fld = lane >> 2, r4 = lane & 3;
+            const int jj = min(it.j + (r4 & 1), g.ny - 1);
+            const int kk = it.kl + (r4 >> 1);
+            const long long vb = ((long long)kk * g.ny + jj) * g.nx + it.seg * 32 + (has_next ? 32 : 31);
+            cp_async8(sg + fld * 136 + r4 * 34 + 32, (fld ? ss : st) + vb);
+        }
+        for (int c = lane; c < U; c += 32) {
+            if (has_prev) cp_async8(ep + c, Xrow - rowlen + c * 32 + 31);
+            else ep[c] = 0.0;
+            if (has_next) cp_async8(en + c, Xrow + rowlen + c * 32);
+            else en[c] = 0.0;
+        }
+    }
+}
+
+template <int N>
+__device__ __forceinline__ void seg_pair_sync(int rw) {
+    if (SegTune<N>::wpr == 1) __syncwarp();
+    else asm volatile("bar.sync %0, %1;\n" ::"r"(1 + rw), "r"(32 * SegTune<N>::wpr) : "memory");
+}
+
+// compute one staged row: outputs (and fused reduction terms) of this warp's classes
+template <int N, int TRANS, int RED, bool JAC>
+__device__ __forceinline__ void seg_compute(const SegParams &prm, const SegGeo &g, const SegItem &it,
+                                            const double *xs, const double *__restrict__ X, double *__restrict__ Y,
+                                            const double *__restrict__ minv, double *__restrict__ zt, int lane,
+                                            int half, RedAcc &ra) {
+    constexpr int U = (N + 1) * (N + 1);
+    constexpr long long rowlen = (long long)U * 32;
+    const int i = it.seg * 32 + lane;
+    SegRow r;
+    r.lane = lane;
+    r.xs = xs + lane;
+    r.eprev = xs + 32 * U;
+    r.enext = r.eprev + U;
+    r.sig = r.enext + U + lane;
+    const double *Xl = X + it.rowbase + lane;
+    r.Xym = it.j > 0 ? Xl - g.nseg * rowlen : nullptr;
+    r.Xyp = it.j < g.ny - 1 ? Xl + g.nseg * rowlen : nullptr;
+    r.Xzm = it.kg > 0 ? Xl - g.plane : nullptr;
+    r.Xzp = it.kg < g.nz - 1 ? Xl + g.plane : nullptr;
+    r.Y = Y + it.rowbase + lane;
+    r.minv = minv ? minv + it.rowbase + lane : nullptr;
+    r.zt = zt ? zt + it.rowbase + lane : nullptr;
+    r.diag = nullptr;
+    r.bx = i == g.nx - 1;
+    r.bx_p = i + 1 == g.nx - 1;
+    r.by = it.j == g.ny - 1;
+    r.bz = it.kg == g.nz - 1;
+    r.by_p = it.j + 1 == g.ny - 1;
+    r.bz_p = it.kg + 1 == g.nz - 1;
+    // warp-uniform: rows away from the last faces and the y/z domain
+    // ends take the mask-free code path
+    const bool interior = it.seg != g.nseg - 1 && it.j >= 1 && it.j <= g.ny - 3 && it.kg >= 1 && it.kg <= g.nz - 3;
+    if (SegTune<N>::wpr == 1) {
+        if (interior) seg_row<N, TRANS, RED, JAC, false, false>(r, prm, ra);
+        else seg_row<N, TRANS, RED, JAC, false, true>(r, prm, ra);
+    } else if (half == 0) {
+        if (interior) seg_half<N, TRANS, 0, RED, JAC, false, false>(r, prm, ra);
+        else seg_half<N, TRANS, 0, RED, JAC, false, true>(r, prm, ra);
+    } else {
+        if (interior) seg_half<N, TRANS, 1, RED, JAC, false, false>(r, prm, ra);
+        else seg_half<N, TRANS, 1, RED, JAC, false, true>(r, prm, ra);
+    }
+}
+
+// one reduction partial per warp and row group (fixed slot): warp tree, lane 0 stores
+template <int N, int RED, bool JAC>
+__device__ __forceinline__ void seg_partial(const SegGeo &g, const SegItem &it, const RedAcc &ra, int lane, int warp,
+                                            double *partials, long long slot_stride, int rb) {
+    if (!RED) return;
+    constexpr int W = SegTune<N>::rows * SegTune<N>::wpr;
+    double v0 = ra.s0, v1 = ra.s1, v2 = (RED == 2 && !JAC) ? ra.s1 : ra.s2;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        v0 += __shfl_down_sync(0xffffffffu, v0, o);
+        v1 += __shfl_down_sync(0xffffffffu, v1, o);
+        v2 += __shfl_down_sync(0xffffffffu, v2, o);
+    }
+    if (lane == 0 && it.jb < g.nyb) {
+        const long long idx = (long long)it.kg * rb + ((long long)it.seg * g.nyb + it.jb) * W + warp;
+        if (RED == 1) partials[idx] = v0;
+        if (RED == 2) { partials[1 * slot_stride + idx] = v1; partials[2 * slot_stride + idx] = v2; }
+    }
+}
+
 template <int N, int TRANS, int RED, bool JAC>
 __global__ void __launch_bounds__(SegTune<N>::threads, SegTune<N>::minb) k_seg(
     const __grid_constant__ SegParams prm, SegGeo g, const double *__restrict__ X, double *__restrict__ Y,
     const double *__restrict__ minv, double *__restrict__ zt, const double *__restrict__ st,
     const double *__restrict__ ss, double *__restrict__ partials, long long slot_stride, int rb, const State *state) {
-    constexpr int U = (N + 1) * (N + 1);
     extern __shared__ __align__(16) double smem[];
     constexpr int WPR = SegTune<N>::wpr;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int rw = warp / WPR, half = warp % WPR;   // row within the CTA, class half
-    // L2-friendly traversal: CTAs march in z inside y-tiles of g.tyb row
-    // blocks, so the z-neighbour rows (k-1, k+1) are still in L2 when read
-    long long bid = blockIdx.x;
-    const int seg = (int)(bid % g.nseg);
-    bid /= g.nseg;
-    const int tyb = min(g.tyb, g.nyb);
-    const int jb_in = (int)(bid % tyb);
-    bid /= tyb;
-    const int kl = g.kl0 + (int)(bid % g.npl) * g.kst;
-    const int jb = (int)(bid / g.npl) * tyb + jb_in;
-    const int j = jb < g.nyb ? jb * SegTune<N>::rows + rw : g.ny;
-    const int kg = g.z0 + kl;
-    constexpr long long rowlen = (long long)U * 32;
+    const SegItem it = seg_item<N>(g, blockIdx.x, rw);
     double *xs = smem + rw * (seg_smem_per_warp<N>() / sizeof(double));
-    double *ep = xs + 32 * U, *en = ep + U, *sg = en + U;
-    RedAcc ra;
-    const long long rowbase = (((long long)kl * g.ny + j) * g.nseg + seg) * rowlen;
-    const double *Xrow = X + rowbase;
-    const bool has_prev = seg > 0, has_next = seg < g.nseg - 1;
-    if (j < g.ny) {
-        // everything the row needs from HBM goes through cp.async (L2 only),
-        // split over the warps of the row: the own row (32*U doubles), the
-        // four sigma_t / sigma_s rows of the staggered site sets, the x+1
-        // sample of lane 31, and the segment-edge values of the neighbours
-#pragma unroll 4
-        for (int q = lane + 32 * half; q < 16 * U; q += 32 * WPR) cp_async16(xs + 2 * q, Xrow + 2 * q);
-        for (int q = lane + 32 * half; q < 128; q += 32 * WPR) {
-            const int rowq = q >> 4, part = (q & 15) * 2, fld = rowq >> 2, r4 = rowq & 3;
-            const int jj = min(j + (r4 & 1), g.ny - 1);
-            const int kk = kl + (r4 >> 1);   // plane nzl exists (edge-replicated at upload)
-            const long long vb = ((long long)kk * g.ny + jj) * g.nx + seg * 32;
-            cp_async16(sg + fld * 136 + r4 * 34 + part, (fld ? ss : st) + vb + part);
-        }
-        if (half == WPR - 1) {
-            if (lane < 8) {   // x+1 sample of lane 31 per sigma row, edge-replicated at nx-1
-                const int fld = lane >> 2, r4 = lane & 3;
-                const int jj = min(j + (r4 & 1), g.ny - 1);
-                const int kk = kl + (r4 >> 1);
-                const long long vb = ((long long)kk * g.ny + jj) * g.nx + seg * 32 + (has_next ? 32 : 31);
-                cp_async8(sg + fld * 136 + r4 * 34 + 32, (fld ? ss : st) + vb);
-            }
-            for (int c = lane; c < U; c += 32) {
-                if (has_prev) cp_async8(ep + c, Xrow - rowlen + c * 32 + 31);
-                else ep[c] = 0.0;
-                if (has_next) cp_async8(en + c, Xrow + rowlen + c * 32);
-                else en[c] = 0.0;
-            }
-        }
+    if (it.j < g.ny) {
+        seg_stage<N>(g, it, xs, X, st, ss, lane, half);
         cp_async_commit();
     }
     // predicated on the solver's stop flag (CTA-uniform), read while the copies are in flight
@@ -232,62 +323,13 @@ __global__ void __launch_bounds__(SegTune<N>::threads, SegTune<N>::minb) k_seg(
         cp_async_wait<0>();
         return;
     }
-    if (j < g.ny) {
-        const int i = seg * 32 + lane;
+    RedAcc ra;
+    if (it.j < g.ny) {
         cp_async_wait<0>();
-        if (WPR == 1) __syncwarp();
-        else asm volatile("bar.sync %0, %1;\n" ::"r"(1 + rw), "r"(32 * WPR) : "memory");
-        SegRow r;
-        r.lane = lane;
-        r.xs = xs + lane;
-        r.eprev = ep;
-        r.enext = en;
-        r.sig = sg + lane;
-        const double *Xl = Xrow + lane;
-        r.Xym = j > 0 ? Xl - g.nseg * rowlen : nullptr;
-        r.Xyp = j < g.ny - 1 ? Xl + g.nseg * rowlen : nullptr;
-        r.Xzm = kg > 0 ? Xl - g.plane : nullptr;
-        r.Xzp = kg < g.nz - 1 ? Xl + g.plane : nullptr;
-        r.Y = Y + rowbase + lane;
-        r.minv = minv ? minv + rowbase + lane : nullptr;
-        r.zt = zt ? zt + rowbase + lane : nullptr;
-        r.diag = nullptr;
-        r.bx = i == g.nx - 1;
-        r.bx_p = i + 1 == g.nx - 1;
-        r.by = j == g.ny - 1;
-        r.bz = kg == g.nz - 1;
-        r.by_p = j + 1 == g.ny - 1;
-        r.bz_p = kg + 1 == g.nz - 1;
-        // warp-uniform: rows away from the last faces and the y/z domain
-        // ends take the mask-free code path
-        const bool interior = seg != g.nseg - 1 && j >= 1 && j <= g.ny - 3 && kg >= 1 && kg <= g.nz - 3;
-        if (WPR == 1) {
-            if (interior) seg_row<N, TRANS, RED, JAC, false, false>(r, prm, ra);
-            else seg_row<N, TRANS, RED, JAC, false, true>(r, prm, ra);
-        } else if (half == 0) {
-            if (interior) seg_half<N, TRANS, 0, RED, JAC, false, false>(r, prm, ra);
-            else seg_half<N, TRANS, 0, RED, JAC, false, true>(r, prm, ra);
-        } else {
-            if (interior) seg_half<N, TRANS, 1, RED, JAC, false, false>(r, prm, ra);
-            else seg_half<N, TRANS, 1, RED, JAC, false, true>(r, prm, ra);
-        }
+        seg_pair_sync<N>(rw);
+        seg_compute<N, TRANS, RED, JAC>(prm, g, it, xs, X, Y, minv, zt, lane, half, ra);
     }
-    if (RED) {
-        // one partial per warp (fixed slot, no CTA barrier): warp tree, lane 0 stores
-        constexpr int W = SegTune<N>::rows * SegTune<N>::wpr;
-        double v0 = ra.s0, v1 = ra.s1, v2 = (RED == 2 && !JAC) ? ra.s1 : ra.s2;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            v0 += __shfl_down_sync(0xffffffffu, v0, o);
-            v1 += __shfl_down_sync(0xffffffffu, v1, o);
-            v2 += __shfl_down_sync(0xffffffffu, v2, o);
-        }
-        if (lane == 0 && jb < g.nyb) {
-            const long long idx = (long long)kg * rb + ((long long)seg * g.nyb + jb) * W + warp;
-            if (RED == 1) partials[idx] = v0;
-            if (RED == 2) { partials[1 * slot_stride + idx] = v1; partials[2 * slot_stride + idx] = v2; }
-        }
-    }
+    seg_partial<N, RED, JAC>(g, it, ra, lane, warp, partials, slot_stride, rb);
 }
 
 template <int N>
