@@ -303,8 +303,14 @@ __device__ __forceinline__ void seg_partial(const SegGeo &g, const SegItem &it, 
     }
 }
 
+#ifdef PN_SEG_MAXNREG
+#define PN_SEG_BOUNDS(N) __maxnreg__(PN_SEG_MAXNREG)
+#else
+#define PN_SEG_BOUNDS(N) __launch_bounds__(SegTune<N>::threads, SegTune<N>::minb)
+#endif
+
 template <int N, int TRANS, int RED, bool JAC>
-__global__ void __launch_bounds__(SegTune<N>::threads, SegTune<N>::minb) k_seg(
+__global__ void PN_SEG_BOUNDS(N) k_seg(
     const __grid_constant__ SegParams prm, SegGeo g, const double *__restrict__ X, double *__restrict__ Y,
     const double *__restrict__ minv, double *__restrict__ zt, const double *__restrict__ st,
     const double *__restrict__ ss, double *__restrict__ partials, long long slot_stride, int rb, const State *state) {
