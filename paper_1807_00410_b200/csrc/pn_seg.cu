@@ -6,6 +6,7 @@
 #include <cmath>
 #include <algorithm>
 #include <cstring>
+#include <cstdlib>
 
 #include "generated/pn_seg_wmap.h"
 #include "pn_seg.cuh"
@@ -72,6 +73,12 @@ int pn_seg_prepare(pn_context *c, cudaStream_t) {
     g.tyb = plane_mb > 12.0 ? std::min(g.nyb, std::max(1, 32 / seg_rows(c->N))) : g.nyb;
     g.plane = c->g.plane;
     g.pvox = c->g.pvox;
+    // bulk (TMA) staging + in-CTA y neighbours where the vector streams from
+    // HBM (measured +2-4 % at 128^3 and 256^3); cp.async where it sits in L2
+    // (64^3: the bulk path measured ~10 % slower).  PNRTE_SEG_BULK=0/1 forces.
+    const double vec_mb = (double)c->g.nzl * c->g.plane * sizeof(double) / 1e6;
+    g.bulk = vec_mb > 96.0;
+    if (const char *e = getenv("PNRTE_SEG_BULK")) g.bulk = atoi(e) != 0;
     sc->ok = true;
     return PN_OK;
 }

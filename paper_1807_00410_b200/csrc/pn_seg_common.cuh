@@ -16,6 +16,8 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include "pn_internal.cuh"
 #include "pn_seg_types.cuh"
 
@@ -33,6 +35,11 @@ struct SegRow {
     const double *diag;                     // stored diagonal row + lane (DIAG_ARRAY)
     int lane;
     bool bx, bx_p, by, bz, by_p, bz_p;      // last-face flags: own voxel, x+1, y+1 row, z+1 row
+    static constexpr bool ysm = false;      // y-neighbour rows always in global memory
+};
+// bulk path: a y-neighbour row may be a staged row of this CTA (shared memory)
+struct SegRowY : SegRow {
+    static constexpr bool ysm = true;
 };
 
 struct RedAcc {
@@ -63,6 +70,34 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
+// Bulk (TMA) copy of the own row: one thread arms an mbarrier with the byte
+// count and issues a single cp.async.bulk of the 32*U doubles (the row is
+// contiguous in the segmented layout); the row's warps wait on the barrier.
+__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long *b, unsigned n) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(n) : "memory");
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long *b, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, unsigned long long *b) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(b))
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_prefetch_l2(const void *src, unsigned bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long *b, unsigned phase) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(b)),
+        "r"(phase)
+        : "memory");
+}
+
 // own-voxel value of comp s as an off-diagonal input (0 on its last face).
 // BND = false: interior row, no face can be hit, no masks are evaluated.
 template <int PS, bool BND>
@@ -84,12 +119,18 @@ __device__ __forceinline__ double nb_x(const SegRow &r, int s) {
     }
 }
 
-template <int PS, int SIDE, bool BND>
-__device__ __forceinline__ double nb_y(const SegRow &r, int s) {
+template <bool YSM>
+__device__ __forceinline__ double ld_row(const double *p) {
+    if constexpr (YSM) return *p;   // generic load: shared (row of this CTA) or global
+    else return __ldg(p);
+}
+
+template <int PS, int SIDE, bool BND, class Row>
+__device__ __forceinline__ double nb_y(const Row &r, int s) {
     const double *p = SIDE < 0 ? r.Xym : r.Xyp;
-    if (!BND) return __ldg(p + s * 32);
+    if (!BND) return ld_row<Row::ysm>(p + s * 32);
     if (!p) return 0.0;
-    const double v = __ldg(p + s * 32);
+    const double v = ld_row<Row::ysm>(p + s * 32);
     const bool pin = ((PS & 1) && r.bx) || ((PS & 2) && SIDE > 0 && r.by_p) || ((PS & 4) && r.bz);
     return pin ? 0.0 : v;
 }
@@ -144,6 +185,11 @@ __device__ __forceinline__ void seg_red_add(RedAcc &ra, double sq) {
     if (RED == 1) ra.s0 += sq;
     if (RED == 2) ra.s1 += sq;
 }
+template <int RED>
+__device__ __forceinline__ void seg_red_sq(RedAcc &ra, double a) {
+    if (RED == 1) ra.s0 = fma(a, a, ra.s0);
+    if (RED == 2) ra.s1 = fma(a, a, ra.s1);
+}
 
 #define W(e) prm.w[e]
 #define DIAG(at, as, c) (DIAG_ARRAY ? __ldg(r.diag + (c) * 32) : fma(-prm.lamp[c], (as), (at)))
@@ -164,7 +210,16 @@ template <int N> struct SegTune {
 
 template <int N>
 __host__ __device__ constexpr size_t seg_smem_per_warp() {
-    return sizeof(double) * ((size_t)32 * (N + 1) * (N + 1) + 2 * (N + 1) * (N + 1) + 2 * 4 * 34);
+    // own row, segment edges, sigma rows, the row's mbarrier (16 B); rounded
+    // up to 128 B so every staged row starts on a shared-memory wavefront
+    // (a misaligned row costs a third wavefront per 256 B warp load)
+    return sizeof(double) * (((size_t)32 * (N + 1) * (N + 1) + 2 * (N + 1) * (N + 1) + 2 * 4 * 34 + 2 + 15) / 16 * 16);
+}
+
+template <int N>
+__device__ __forceinline__ unsigned long long *seg_bar(double *xs) {
+    constexpr int U = (N + 1) * (N + 1);
+    return reinterpret_cast<unsigned long long *>(xs + 32 * U + 2 * U + 2 * 4 * 34);
 }
 
 // one row of one CTA row-group ("virtual block" vb of the tiled traversal):
@@ -192,11 +247,13 @@ __device__ __forceinline__ SegItem seg_item(const SegGeo &g, long long vb, int r
     return it;
 }
 
-// issue the row's cp.async copies into buffer xs (split over the warps of
-// the row): the own row (32*U doubles), the four sigma_t / sigma_s rows of
-// the staggered site sets, the x+1 sample of lane 31, and the segment-edge
-// values of the neighbours.  Everything from HBM goes through L2 only.
-template <int N>
+// issue the row's copies into buffer xs (split over the warps of the row):
+// the own row (32*U doubles), the four sigma_t / sigma_s rows of the
+// staggered site sets, the x+1 sample of lane 31, and the segment-edge values
+// of the neighbours.  Everything from HBM goes through L2 only.  TMA: the own
+// row is one bulk copy completing on the row's mbarrier (initialised by the
+// kernel before the CTA barrier); otherwise cp.async by all the row's lanes.
+template <int N, bool TMA>
 __device__ __forceinline__ void seg_stage(const SegGeo &g, const SegItem &it, double *xs, const double *__restrict__ X,
                                           const double *__restrict__ st, const double *__restrict__ ss, int lane,
                                           int half) {
@@ -206,8 +263,16 @@ __device__ __forceinline__ void seg_stage(const SegGeo &g, const SegItem &it, do
     double *ep = xs + 32 * U, *en = ep + U, *sg = en + U;
     const double *Xrow = X + it.rowbase;
     const bool has_prev = it.seg > 0, has_next = it.seg < g.nseg - 1;
+    if constexpr (TMA) {
+        if (half == 0 && lane == 0) {
+            unsigned long long *bar = seg_bar<N>(xs);
+            mbar_expect_tx(bar, (unsigned)(rowlen * sizeof(double)));
+            bulk_g2s(xs, Xrow, (unsigned)(rowlen * sizeof(double)), bar);
+        }
+    } else {
 #pragma unroll 4
-    for (int q = lane + 32 * half; q < 16 * U; q += 32 * WPR) cp_async16(xs + 2 * q, Xrow + 2 * q);
+        for (int q = lane + 32 * half; q < 16 * U; q += 32 * WPR) cp_async16(xs + 2 * q, Xrow + 2 * q);
+    }
     for (int q = lane + 32 * half; q < 128; q += 32 * WPR) {
         const int rowq = q >> 4, part = (q & 15) * 2, fld = rowq >> 2, r4 = rowq & 3;
         const int jj = min(it.j + (r4 & 1), g.ny - 1);
@@ -239,15 +304,16 @@ __device__ __forceinline__ void seg_pair_sync(int rw) {
 }
 
 // compute one staged row: outputs (and fused reduction terms) of this warp's classes
-template <int N, int TRANS, int RED, bool JAC>
+template <int N, int TRANS, int RED, bool JAC, bool TMA>
 __device__ __forceinline__ void seg_compute(const SegParams &prm, const SegGeo &g, const SegItem &it,
                                             const double *xs, const double *__restrict__ X, double *__restrict__ Y,
+                                            int rw,
                                             const double *__restrict__ minv, double *__restrict__ zt, int lane,
                                             int half, RedAcc &ra) {
     constexpr int U = (N + 1) * (N + 1);
     constexpr long long rowlen = (long long)U * 32;
     const int i = it.seg * 32 + lane;
-    SegRow r;
+    std::conditional_t<TMA, SegRowY, SegRow> r;
     r.lane = lane;
     r.xs = xs + lane;
     r.eprev = xs + 32 * U;
@@ -256,6 +322,11 @@ __device__ __forceinline__ void seg_compute(const SegParams &prm, const SegGeo &
     const double *Xl = X + it.rowbase + lane;
     r.Xym = it.j > 0 ? Xl - g.nseg * rowlen : nullptr;
     r.Xyp = it.j < g.ny - 1 ? Xl + g.nseg * rowlen : nullptr;
+    if constexpr (TMA) {   // y neighbours inside the CTA: the adjacent staged rows
+        constexpr int SW = (int)(seg_smem_per_warp<N>() / sizeof(double));
+        if (rw > 0) r.Xym = xs - SW + lane;
+        if (rw < SegTune<N>::rows - 1 && r.Xyp) r.Xyp = xs + SW + lane;
+    }
     r.Xzm = it.kg > 0 ? Xl - g.plane : nullptr;
     r.Xzp = it.kg < g.nz - 1 ? Xl + g.plane : nullptr;
     r.Y = Y + it.rowbase + lane;
@@ -309,31 +380,59 @@ __device__ __forceinline__ void seg_partial(const SegGeo &g, const SegItem &it, 
 #define PN_SEG_BOUNDS(N) __launch_bounds__(SegTune<N>::threads, SegTune<N>::minb)
 #endif
 
-template <int N, int TRANS, int RED, bool JAC>
+#ifndef PN_SEG_PF
+#define PN_SEG_PF 148   // L2 prefetch distance in CTAs (bulk path); 0 disables
+#endif
+
+// TMA = true ("bulk" path, HBM-sized slabs): own rows by cp.async.bulk on
+// per-row mbarriers, y neighbours inside the CTA read from the adjacent staged
+// rows, and the row of the CTA PN_SEG_PF places ahead prefetched into L2.
+// TMA = false (L2-resident slabs, where the bulk path measured slower):
+// cp.async staging, all y/z neighbours from L2.
+template <int N, int TRANS, int RED, bool JAC, bool TMA>
 __global__ void PN_SEG_BOUNDS(N) k_seg(
     const __grid_constant__ SegParams prm, SegGeo g, const double *__restrict__ X, double *__restrict__ Y,
     const double *__restrict__ minv, double *__restrict__ zt, const double *__restrict__ st,
     const double *__restrict__ ss, double *__restrict__ partials, long long slot_stride, int rb, const State *state) {
     extern __shared__ __align__(16) double smem[];
     constexpr int WPR = SegTune<N>::wpr;
+    constexpr int SW = (int)(seg_smem_per_warp<N>() / sizeof(double));
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int rw = warp / WPR, half = warp % WPR;   // row within the CTA, class half
     const SegItem it = seg_item<N>(g, blockIdx.x, rw);
-    double *xs = smem + rw * (seg_smem_per_warp<N>() / sizeof(double));
+    double *xs = smem + rw * SW;
+    if constexpr (TMA) {   // every row's barrier exists before any warp waits on it
+        if (threadIdx.x < SegTune<N>::rows) mbar_init(seg_bar<N>(smem + threadIdx.x * SW), 1);
+        __syncthreads();
+    }
     if (it.j < g.ny) {
-        seg_stage<N>(g, it, xs, X, st, ss, lane, half);
+        seg_stage<N, TMA>(g, it, xs, X, st, ss, lane, half);
         cp_async_commit();
+    }
+    if constexpr (TMA && PN_SEG_PF > 0) {
+        // warm L2 with the row the CTA PN_SEG_PF places later will stage
+        // (about half a CTA lifetime ahead at two resident CTAs per SM)
+        if (lane == 0 && half == WPR - 1 && blockIdx.x + PN_SEG_PF < gridDim.x) {
+            const SegItem nx = seg_item<N>(g, blockIdx.x + PN_SEG_PF, rw);
+            if (nx.j < g.ny) bulk_prefetch_l2(X + nx.rowbase, (unsigned)((N + 1) * (N + 1) * 32 * sizeof(double)));
+        }
     }
     // predicated on the solver's stop flag (CTA-uniform), read while the copies are in flight
     if (state && seg_stopped(state)) {
         cp_async_wait<0>();
+        if (TMA && it.j < g.ny && half == 0 && lane == 0) mbar_wait(seg_bar<N>(xs), 0);   // no copy outlives the CTA
         return;
     }
     RedAcc ra;
     if (it.j < g.ny) {
         cp_async_wait<0>();
         seg_pair_sync<N>(rw);
-        seg_compute<N, TRANS, RED, JAC>(prm, g, it, xs, X, Y, minv, zt, lane, half, ra);
+        if constexpr (TMA) {   // own row, and the CTA's adjacent rows serving as y neighbours
+            mbar_wait(seg_bar<N>(xs), 0);
+            if (rw > 0) mbar_wait(seg_bar<N>(xs - SW), 0);
+            if (rw < SegTune<N>::rows - 1 && it.j + 1 < g.ny) mbar_wait(seg_bar<N>(xs + SW), 0);
+        }
+        seg_compute<N, TRANS, RED, JAC, TMA>(prm, g, it, xs, X, Y, rw, minv, zt, lane, half, ra);
     }
     seg_partial<N, RED, JAC>(g, it, ra, lane, warp, partials, slot_stride, rb);
 }
@@ -347,14 +446,20 @@ int seg_launch(const SegParams &prm, const SegGeo &g, int trans, int red, bool j
     dim3 grid((unsigned)((long long)g.nseg * g.tyb * g.npl * ytiles)), block(SegTune<N>::threads);
     const size_t smem = rows * seg_smem_per_warp<N>();
     if (g.nyb != (g.ny + rows - 1) / rows) { set_error("segmented launch: row blocking mismatch"); return PN_ERR_INVALID; }
-#define PN_SEG_GO(T, R, J)                                                                                   \
-    do {                                                                                                     \
-        static bool cfg_done = false;                                                                        \
-        if (!cfg_done) {                                                                                     \
-            cudaFuncSetAttribute(k_seg<N, T, R, J>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-            cfg_done = true;                                                                                 \
-        }                                                                                                    \
-        k_seg<N, T, R, J><<<grid, block, smem, s>>>(prm, g, x, y, minv, zt, st, ss, partials, slot_stride, rb, state); \
+#define PN_SEG_GO2(T, R, J, B)                                                                                  \
+    do {                                                                                                        \
+        static bool cfg_done = false;                                                                           \
+        if (!cfg_done) {                                                                                        \
+            cudaFuncSetAttribute(k_seg<N, T, R, J, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+            cfg_done = true;                                                                                    \
+        }                                                                                                       \
+        k_seg<N, T, R, J, B><<<grid, block, smem, s>>>(prm, g, x, y, minv, zt, st, ss, partials, slot_stride, rb, \
+                                                       state);                                                  \
+    } while (0)
+#define PN_SEG_GO(T, R, J)                     \
+    do {                                       \
+        if (g.bulk) PN_SEG_GO2(T, R, J, true); \
+        else PN_SEG_GO2(T, R, J, false);       \
     } while (0)
     if (!trans) {
         if (red == 1) PN_SEG_GO(0, 1, false);
@@ -367,6 +472,7 @@ int seg_launch(const SegParams &prm, const SegGeo &g, int trans, int red, bool j
             PN_SEG_GO(1, 0, false);
         }
     }
+#undef PN_SEG_GO2
 #undef PN_SEG_GO
     PN_CUDA(cudaGetLastError());
     return PN_OK;

@@ -27,6 +27,7 @@ struct SegGeo {
     int U, nx, ny, nz, z0, nzl, nseg, nyb;
     int tyb;                 // row blocks per y-tile of the CTA traversal
     int kl0, npl, kst;       // local planes kl0 + i*kst, i < npl, computed by one launch
+    int bulk;                // 1: bulk (TMA) staging path, for slabs far larger than L2
     long long plane, pvox;
 };
 

@@ -163,3 +163,32 @@ def test_config_faithful_bit_identical_to_reference(idx, golden):
     floor = {1: 4.6e-8, 2: 6e-16}[idx]
     assert rel(xf.cpu().numpy(), x.cpu().numpy()) <= max(FIELD_RTOL, 4 * floor)
     assert rf.converged and rf.normal_residual <= cfg.tol * 1.01
+
+
+@pytest.mark.parametrize("N", [1, 2, 3, 5, 7])
+def test_bulk_staging_path_bit_identical(N, monkeypatch):
+    """The bulk (TMA) staging path -- own rows by cp.async.bulk, y neighbours
+    from the CTA's adjacent staged rows, L2 prefetch -- is selected for slabs
+    far above L2; forced on here at small sizes it must give the same bits as
+    the cp.async path (same arithmetic, only where operands come from), for
+    both products, the fused reductions and Jacobi, and against the oracle."""
+    from oracle.oracle import StencilOracle
+    from paper_1807_00410_b200.solver import PnContext
+    res = (64, 11, 7)
+    spec = rand_spec(N, res, 77 + N)
+    t = build_tables(N)
+    out = {}
+    for bulk in ("0", "1"):
+        monkeypatch.setenv("PNRTE_SEG_BULK", bulk)
+        c = PnContext(t, res, spec.h)
+        c.set_fields(spec)
+        x = probe_vector(c.R_local)
+        ys = [c.apply(x, tr, "fast").cpu().numpy() for tr in (0, 1)]
+        sols = [c.solve(tol=1e-300, max_iter=25, jacobi=j, mode="fast")[0].cpu().numpy() for j in (False, True)]
+        out[bulk] = ys + sols
+    for a, b in zip(out["0"], out["1"]):
+        assert a.tobytes() == b.tobytes()
+    o = StencilOracle(t, spec)
+    x = probe_vector(o.R)
+    assert rel(out["1"][0], o.apply(x)) <= FAST_APPLY_RTOL
+    assert rel(out["1"][1], o.apply(x, True)) <= FAST_APPLY_RTOL
