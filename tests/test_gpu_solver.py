@@ -150,10 +150,15 @@ def _group(tables, spec, n_slabs):
 
 @pytest.mark.parametrize("N,res,slabs", [(1, (32, 8, 8), 2), (3, (32, 6, 8), 4), (7, (32, 4, 4), 2), (5, (32, 8, 12), 3), (7, (64, 8, 10), 2),
                                          (3, (7, 5, 6), 3)])
-def test_loopback_slabs_match_single_slab(N, res, slabs):
+@pytest.mark.parametrize("bulk", ["0", "1"])
+def test_loopback_slabs_match_single_slab(N, res, slabs, bulk, monkeypatch):
     """z-slab decomposition (halo planes + all-gathered plane partials) gives
-    the single-GPU result bit for bit, for the operator and the full solve."""
+    the single-GPU result bit for bit, for the operator and the full solve;
+    with the segmented kernel's cp.async (bulk=0) and bulk/TMA (bulk=1)
+    staging paths (the plane-range launches of the interior / boundary planes
+    differ between the two)."""
     import torch
+    monkeypatch.setenv("PNRTE_SEG_BULK", bulk)
     from paper_1807_00410_b200 import _lib
     from paper_1807_00410_b200.solver import PnContext
     spec = rand_spec(N, res, 31)
