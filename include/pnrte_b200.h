@@ -215,8 +215,10 @@ int pn_group_apply(pn_context **ctxs, int32_t n, int32_t transpose, int32_t mode
                    const double **x, double **y, void *stream);
 
 /* Kernel-level timing hooks for bench.py: run `reps` back-to-back fast
- * applies (or fused CG iterations, what = 1) on internal buffers and return
- * the average device time per launch in milliseconds. */
+ * operations on internal buffers and return the average device time per
+ * launch in milliseconds.  what: 0 applies (A / A^T alternating), 1 fused CG
+ * iterations, 2 applies with the fused reductions, 3 applies predicated on the
+ * stop flag, 4 the r update (r -= alpha w, ||r||^2), 5 the x / p update. */
 int pn_bench(pn_context *ctx, int32_t what, int32_t reps, double *ms_per, void *stream);
 
 #ifdef __cplusplus

@@ -13,6 +13,7 @@
 // contracted into FMAs (numpy / sparsetools do mul then add).  Kernels that
 // may use FMA live in pn_seg.cu.
 #include <cuda_runtime.h>
+#include <cstdint>
 #include <math.h>
 
 #include "pn_internal.cuh"
@@ -335,8 +336,37 @@ __global__ void __launch_bounds__(256) k_r(Geo g, double *__restrict__ r, const 
     const long long base = (long long)kl * g.plane;
     const double alpha = st->alpha;
     double acc = 0.0;
-    for (long long rp = r0 + threadIdx.x; rp < r1; rp += blockDim.x) {
-        const long long i = base + rp;
+    long long i0 = base + r0, i1 = base + r1;
+#ifndef PN_VEC_SCALAR
+    // paired (16 B) accesses when every z-plane starts 16 B-aligned (even plane
+    // length, aligned buffers): the element-to-thread map then depends on the
+    // plane-local index only, so the partial sums do not depend on the slab
+    // decomposition.  A leading odd element is done first.
+    const bool paired = !(g.plane & 1) && !((reinterpret_cast<uintptr_t>(r) | reinterpret_cast<uintptr_t>(w)) & 15);
+    if (paired && (i0 & 1) && i0 < i1) {
+        if (threadIdx.x == 0) {
+            const double rv = fma(-alpha, w[i0], r[i0]);
+            r[i0] = rv;
+            acc = fma(rv, rv, acc);
+        }
+        ++i0;
+    }
+    const long long np = paired ? (i1 - i0) >> 1 : 0;
+    double2 *r2 = reinterpret_cast<double2 *>(r + i0);
+    const double2 *w2 = reinterpret_cast<const double2 *>(w + i0);
+#pragma unroll 4
+    for (long long q = threadIdx.x; q < np; q += blockDim.x) {
+        const double2 wv = w2[q];
+        double2 rv = r2[q];
+        rv.x = fma(-alpha, wv.x, rv.x);
+        rv.y = fma(-alpha, wv.y, rv.y);
+        r2[q] = rv;
+        acc = fma(rv.x, rv.x, acc);
+        acc = fma(rv.y, rv.y, acc);
+    }
+    i0 += 2 * np;
+#endif
+    for (long long i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
         const double rv = fma(-alpha, w[i], r[i]);
         r[i] = rv;
         acc = fma(rv, rv, acc);
@@ -359,8 +389,45 @@ __global__ void __launch_bounds__(256) k_xp(Geo g, double *__restrict__ x, doubl
     const long long r1 = min(g.plane, r0 + chunk);
     const long long base = (long long)kl * g.plane;
     const double alpha = st->alpha, beta = st->beta;
-    for (long long rp = r0 + threadIdx.x; rp < r1; rp += blockDim.x) {
-        const long long i = base + rp;
+    long long i0 = base + r0, i1 = base + r1;
+#ifndef PN_VEC_SCALAR
+    const bool paired = !(g.plane & 1) && !((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(p) |
+                                             reinterpret_cast<uintptr_t>(zt)) & 15);
+    if (paired && (i0 & 1) && i0 < i1) {
+        if (threadIdx.x == 0) {
+            const double pv = p[i0];
+            x[i0] = fma(alpha, pv, x[i0]);
+            if (upd_p) p[i0] = fma(beta, pv, zt[i0]);
+        }
+        ++i0;
+    }
+    const long long np = paired ? (i1 - i0) >> 1 : 0;
+    double2 *x2 = reinterpret_cast<double2 *>(x + i0);
+    double2 *p2 = reinterpret_cast<double2 *>(p + i0);
+    const double2 *z2 = reinterpret_cast<const double2 *>(zt + i0);
+    if (upd_p) {
+#pragma unroll 4
+        for (long long q = threadIdx.x; q < np; q += blockDim.x) {
+            const double2 pv = p2[q], zv = z2[q];
+            double2 xv = x2[q];
+            xv.x = fma(alpha, pv.x, xv.x);
+            xv.y = fma(alpha, pv.y, xv.y);
+            x2[q] = xv;
+            p2[q] = make_double2(fma(beta, pv.x, zv.x), fma(beta, pv.y, zv.y));
+        }
+    } else {
+#pragma unroll 4
+        for (long long q = threadIdx.x; q < np; q += blockDim.x) {
+            const double2 pv = p2[q];
+            double2 xv = x2[q];
+            xv.x = fma(alpha, pv.x, xv.x);
+            xv.y = fma(alpha, pv.y, xv.y);
+            x2[q] = xv;
+        }
+    }
+    i0 += 2 * np;
+#endif
+    for (long long i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
         const double pv = p[i];
         x[i] = fma(alpha, pv, x[i]);
         if (upd_p) p[i] = fma(beta, pv, zt[i]);

@@ -957,9 +957,10 @@ int pn_bench(pn_context *c, int32_t what, int32_t reps, double *ms_per, void *st
         PN_TRY(group_vec(cs, V_COPY, &pn_context::r, &pn_context::bs, nullptr, false, s));
         c->bench_ready = true;
     }
-    if (what == 1 || what == 3) {
+    if (what == 1 || what == 3 || what == 4 || what == 5) {
         State h{};
         h.tol = 1e-300; h.primal_tol = -1; h.max_iter = 1LL << 40; h.rho = 1.0; h.norm_b = 1.0; h.norm_atb = 1.0;
+        h.alpha = 1e-3; h.beta = 0.5; h.xupd = what == 5;
         PN_CUDA(cudaMemcpyAsync(c->state, &h, sizeof(State), cudaMemcpyHostToDevice, s));
     }
     PN_CUDA(cudaEventRecord(e0, s));
@@ -967,6 +968,8 @@ int pn_bench(pn_context *c, int32_t what, int32_t reps, double *ms_per, void *st
         if (what == 0) PN_TRY(group_apply(cs, k & 1, 0, &pn_context::p, &pn_context::w, 0, false, false, s, seg));
         else if (what == 2) PN_TRY(group_apply(cs, k & 1, 0, &pn_context::p, &pn_context::w, (k & 1) ? 2 : 1, false, false, s, seg));
         else if (what == 3) PN_TRY(group_apply(cs, k & 1, 0, &pn_context::p, &pn_context::w, 0, false, true, s, seg));
+        else if (what == 4) PN_TRY(launch_r_update(c, s));                  // r -= alpha w, ||r||^2 partials
+        else if (what == 5) PN_TRY(launch_xp_update(c, c->z.p, s));        // x += alpha p ; p = z + beta p
         else PN_TRY(iteration(cs, &o, false, seg, s));
     }
     PN_CUDA(cudaEventRecord(e1, s));
