@@ -52,7 +52,7 @@ def build(verbose=False, force=False):
     from . import codegen
     codegen.generate()
     inc, libdir = _nccl_dirs()
-    OUT_DIR.mkdir(exist_ok=True)
+    OUT_DIR.mkdir(parents=True, exist_ok=True)
     objs = []
     jobs = []
     deps = list(CSRC.glob("*.cuh")) + list((CSRC / "generated").glob("*.cuh")) + list((CSRC / "generated").glob("*.h"))
