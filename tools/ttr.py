@@ -14,6 +14,8 @@ for idx in [int(v) for v in a.configs.split(",")]:
     spec = solve_spec(cfg)
     c = PnContext(build_tables(cfg.N), spec.res, spec.h)
     t0 = time.perf_counter(); c.set_fields(spec); torch.cuda.synchronize(); t_setup = time.perf_counter() - t0
+    c.solve(tol=cfg.tol, max_iter=5)   # warm-up as in bench.py: module loading, graph capture
+    torch.cuda.synchronize()
     t0 = time.perf_counter()
     x, rep = c.solve(tol=cfg.tol, max_iter=min(cfg.max_iter, a.max_iter))
     torch.cuda.synchronize(); t = time.perf_counter() - t0
