@@ -44,7 +44,7 @@ def _flags(src, inc):
          "-I", str(CSRC), "-I", str(inc), *ARCH]
     f += EXTRA
     if src.name in ("pn_kernels.cu", "pn_csr.cu", "pn_post.cu"):
-        f.append("-fmad=false")
+        f += ["-fmad=false", "-Xcompiler", "-ffp-contract=off"]   # device and host twins (k_setup constants)
     return f
 
 

@@ -167,6 +167,14 @@ struct pn_context {
     void *seg = nullptr;
     pn::Buf bs;                   // RHS in the solve layout
     std::vector<double> h_aw, h_tw;
+    // residual (RHS) term program on the host: comps whose terms use only
+    // constant factors get their value once per setup (k_setup skips them)
+    std::vector<int> h_rptr, h_hascoef, h_nf, h_tf;
+    std::vector<double> h_tcoef;
+    std::vector<int> h_rmode;       // per comp: 1 = constant RHS
+    std::vector<double> h_rconst;   // per comp: that constant (exact device arithmetic)
+    int *d_rmode = nullptr;
+    double *d_rconst = nullptr;
 
     // generic CSR system instead of a stencil (pn_create_csr)
     bool is_csr = false;

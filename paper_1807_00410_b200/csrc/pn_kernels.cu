@@ -98,7 +98,8 @@ __device__ __forceinline__ int boundary_bits(const Geo &g, int i, int j, int kg)
 // Grid (row blocks of a plane, planes): index arithmetic stays 32-bit inside a
 // plane (a plane holds < 2^31 rows), 64-bit divisions per row made the kernel
 // integer-bound (8.6 GB of RHS in 35 ms at config 4).
-__global__ void k_setup(Tables T, Fields F, Geo g, double *diag, double *rhs, int pin) {
+__global__ void k_setup(Tables T, Fields F, Geo g, double *diag, double *rhs, int pin, const int *__restrict__ rmode,
+                        const double *__restrict__ rconst) {
     const int kl = blockIdx.y;
     const unsigned rp = blockIdx.x * blockDim.x + threadIdx.x;   // row within the plane
     if (rp >= (unsigned)g.plane) return;
@@ -111,8 +112,41 @@ __global__ void k_setup(Tables T, Fields F, Geo g, double *diag, double *rhs, in
     if (diag) diag[row] = eval_terms(T, F, g, T.d_ptr[c], T.d_ptr[c + 1], i, j, kl);
     if (rhs) {
         double r = 0.0;
-        if (T.r_ptr[c + 1] > T.r_ptr[c]) r = -eval_terms(T, F, g, T.r_ptr[c], T.r_ptr[c + 1], i, j, kl);
+        if (rmode[c]) r = rconst[c];
+        else if (T.r_ptr[c + 1] > T.r_ptr[c]) r = -eval_terms(T, F, g, T.r_ptr[c], T.r_ptr[c + 1], i, j, kl);
         rhs[row] = (pin && (T.par[c] & bb)) ? 0.0 : r;
+    }
+}
+
+// Host twin of eval_terms for comps whose factors are all constants (missing
+// or uniform fields): the same multiplies and adds in the same order, IEEE
+// double on both sides (this unit is compiled without contraction), so the
+// constant equals what every thread would compute.
+static void rhs_constants(pn_context *c) {
+    const int U = c->U;
+    c->h_rmode.assign(U, 0);
+    c->h_rconst.assign(U, 0.0);
+    for (int comp = 0; comp < U; ++comp) {
+        const int t0 = c->h_rptr[comp], t1 = c->h_rptr[comp + 1];
+        bool konst = true;
+        double acc = 0.0;
+        for (int t = t0; t < t1 && konst; ++t) {
+            auto fs = [&](int slot, bool &ok) {
+                const int kd = c->f.kind[slot];
+                if (kd == 2) ok = false;
+                return kd == 1 ? c->f.scalar[slot] : 0.0;
+            };
+            const int nf = c->h_nf[t];
+            int f = 0;
+            double v;
+            if (c->h_hascoef[t]) v = c->h_tcoef[t];
+            else { v = fs(c->h_tf[2 * t], konst); f = 1; }
+            for (; f < nf; ++f) v = v * fs(c->h_tf[2 * t + f], konst);
+            acc = (t == t0) ? v : acc + v;
+        }
+        if (!konst) continue;
+        c->h_rmode[comp] = 1;
+        c->h_rconst[comp] = t1 > t0 ? -acc : 0.0;
     }
 }
 
@@ -121,7 +155,12 @@ int launch_setup(pn_context *c, bool want_diag, bool want_rhs, cudaStream_t s, d
     if (c->g.plane >= (1LL << 31)) { set_error("setup: z-plane too large"); return PN_ERR_UNSUPPORTED; }
     dim3 grid((unsigned)((c->g.plane + bs - 1) / bs), (unsigned)c->g.nzl);
     double *rhs = want_rhs ? (rhs_out ? rhs_out : c->b.p) : nullptr;
-    k_setup<<<grid, bs, 0, s>>>(c->tb, c->f, c->g, want_diag ? c->diag : nullptr, rhs, pin);
+    if (want_rhs) {
+        rhs_constants(c);
+        PN_CUDA(cudaMemcpyAsync(c->d_rmode, c->h_rmode.data(), c->U * sizeof(int), cudaMemcpyHostToDevice, s));
+        PN_CUDA(cudaMemcpyAsync(c->d_rconst, c->h_rconst.data(), c->U * sizeof(double), cudaMemcpyHostToDevice, s));
+    }
+    k_setup<<<grid, bs, 0, s>>>(c->tb, c->f, c->g, want_diag ? c->diag : nullptr, rhs, pin, c->d_rmode, c->d_rconst);
     PN_CUDA(cudaGetLastError());
     c->launches++;
     return PN_OK;

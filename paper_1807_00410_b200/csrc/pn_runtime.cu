@@ -188,6 +188,11 @@ int pn_create(const pn_desc *d, pn_context **out) {
     c->h_lidx.assign(d->lidx, d->lidx + d->U);
     c->h_aw.assign(d->a_w, d->a_w + d->n_a);
     c->h_tw.assign(d->t_w, d->t_w + d->n_t);
+    c->h_rptr.assign(d->r_ptr, d->r_ptr + d->U + 1);
+    c->h_hascoef.assign(d->term_hascoef, d->term_hascoef + d->n_terms);
+    c->h_nf.assign(d->term_nf, d->term_nf + d->n_terms);
+    c->h_tf.assign(d->term_f, d->term_f + 2 * (size_t)d->n_terms);
+    c->h_tcoef.assign(d->term_coef, d->term_coef + d->n_terms);
     int st = PN_OK;
     Tables &t = c->tb;
     auto ci = [&](const int **dst, const int32_t *src, size_t n) {
@@ -219,7 +224,9 @@ int pn_create(const pn_desc *d, pn_context **out) {
         c->vec_bx = std::max(1, pn_seg_red_blocks(c) / warps);   // segments x row blocks per plane
         c->red_bx = pn_seg_red_blocks(c);
     }
-    st = dalloc(c, &c->partials, (size_t)RED_SLOTS * g.nz * c->red_bx);
+    if (st == PN_OK) st = dalloc(c, &c->d_rmode, U);
+    if (st == PN_OK) st = dalloc(c, &c->d_rconst, U);
+    st = st == PN_OK ? dalloc(c, &c->partials, (size_t)RED_SLOTS * g.nz * c->red_bx) : st;
     if (st == PN_OK) st = dalloc(c, &c->plane_sums, (size_t)RED_SLOTS * g.nz);
     if (st == PN_OK) st = dalloc(c, &c->ddot_chunks, 4 * 64);
     if (st == PN_OK) st = dalloc(c, &c->state, 1);
