@@ -140,6 +140,7 @@ struct pn_context {
     int vec_bx = 0;               // blocks per plane of the vector / table / dot kernels
     double *partials = nullptr;   // [RED_SLOTS][nz][red_bx] block partials (global plane index)
     double *plane_sums = nullptr; // [RED_SLOTS][nz] level-1 sums (all-gathered across ranks)
+    unsigned *counter = nullptr;  // finished-block count of the fused plane-sum / scalar launch
     double *ddot_chunks = nullptr;// faithful ddot chunk results [4][64]
     pn::State *state = nullptr;   // device
     pn::State *h_state = nullptr; // pinned host mirror
@@ -198,6 +199,8 @@ int launch_apply_faithful(pn_context *c, int trans, int squared, const double *x
 int launch_r_update(pn_context *c, cudaStream_t s);
 int launch_xp_update(pn_context *c, const double *zt, cudaStream_t s);
 int launch_plane_sums(pn_context *c, int mask, int cnt, cudaStream_t s);
+// single-slab: plane sums of `mask` (slot 3 with cnt3 partials) + scalar step `which` in one launch
+int launch_plane_sums_scalar(pn_context *c, int mask, int cnt, int cnt3, int which, cudaStream_t s);
 int launch_dot(pn_context *c, const double *a, const double *b, int slot, cudaStream_t s, bool gated = false);
 int launch_ddot_emul(pn_context *c, const double *a, const double *b, long long n, int slot, int threads,
                      int kernel, cudaStream_t s, bool gated = false);

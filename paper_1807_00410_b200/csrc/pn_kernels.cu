@@ -654,7 +654,8 @@ struct ScalarArgs {
 __device__ double sum_slot(const ScalarArgs &a, int slot, double *sh) {
     const double *p = a.partials + slot * a.n_part;   // plane sums of the slot
     double acc = 0.0;
-    for (long long i = threadIdx.x; i < a.n_part; i += blockDim.x) acc = __dadd_rn(acc, p[i]);
+    // L2 loads: in the fused plane-sum step the values were written by other blocks of the same grid
+    for (long long i = threadIdx.x; i < a.n_part; i += blockDim.x) acc = __dadd_rn(acc, __ldcg(p + i));
     sh[threadIdx.x] = acc;
     __syncthreads();
     for (int o = blockDim.x / 2; o > 0; o >>= 1) {
@@ -674,8 +675,7 @@ __device__ double chunk_sum(const ScalarArgs &a, int slot) {
     return d;
 }
 
-__global__ void __launch_bounds__(256) k_scalar(int which, ScalarArgs a, State *st) {
-    __shared__ double sh[256];
+__device__ void scalar_step(int which, const ScalarArgs &a, State *st, double *sh) {
     if (which == S_ALPHA && threadIdx.x == 0) st->xupd = 0;   // previous iteration's x update has run
     if ((which == S_ALPHA || which == S_BETA) && stopped(st)) return;
     // slots each step consumes: 0 generic / ww, 1 zz, 2 zzt, 3 rr
@@ -724,6 +724,71 @@ __global__ void __launch_bounds__(256) k_scalar(int which, ScalarArgs a, State *
         }
         case S_FINAL: st->zz = v[0]; st->rr = v[3]; break;
     }
+}
+
+__global__ void __launch_bounds__(256) k_scalar(int which, ScalarArgs a, State *st) {
+    __shared__ double sh[256];
+    scalar_step(which, a, st, sh);
+}
+
+// Single-slab fast solves: the level-1 plane sums of the masked slots (slot 3
+// with its own partial count) and, in the block that finishes last, the
+// scalar step -- one launch instead of two (three at the beta step), with the
+// same fixed summation trees, so the result is bit-identical to the separate
+// kernels.  counter returns to 0 for the next launch.
+__global__ void __launch_bounds__(256) k_plane_sums_scalar(const double *__restrict__ partials, double *plane_sums,
+                                                           long long slot_stride, int rb, int nz, int z0, int mask,
+                                                           int cnt, int cnt3, int which, ScalarArgs a, State *st,
+                                                           unsigned *counter) {
+    __shared__ double sh[256];
+    __shared__ bool last;
+    const int slot = blockIdx.y;
+    if (mask >> slot & 1) {
+        const int kg = z0 + blockIdx.x;
+        const double *p = partials + slot * slot_stride + (long long)kg * rb;
+        const int n = slot == 3 ? cnt3 : cnt;
+        double acc = 0.0;
+        for (int i = threadIdx.x; i < n; i += blockDim.x) acc = __dadd_rn(acc, p[i]);
+        sh[threadIdx.x] = acc;
+        __syncthreads();
+        for (int o = 128; o > 0; o >>= 1) {
+            if (threadIdx.x < o) sh[threadIdx.x] = __dadd_rn(sh[threadIdx.x], sh[threadIdx.x + o]);
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) plane_sums[slot * nz + kg] = sh[0];
+    }
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned done = atomicAdd(counter, 1u);
+        last = done == gridDim.x * gridDim.y - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    scalar_step(which, a, st, sh);
+    if (threadIdx.x == 0) *counter = 0u;
+}
+
+static ScalarArgs scalar_args(pn_context *c, int faithful, int blas_threads) {
+    ScalarArgs a;
+    a.partials = c->plane_sums;
+    a.n_part = c->g.nz;
+    a.chunks = c->ddot_chunks;
+    a.faithful = faithful;
+    a.nchunks = (c->R_l() <= 10000 || blas_threads <= 1) ? 1 : blas_threads;
+    a.hist_n = c->hist_n;
+    a.hist_p = c->hist_p;
+    a.hist_len = c->hist_len;
+    return a;
+}
+
+int launch_plane_sums_scalar(pn_context *c, int mask, int cnt, int cnt3, int which, cudaStream_t s) {
+    dim3 grid(c->g.nzl, RED_SLOTS);
+    k_plane_sums_scalar<<<grid, 256, 0, s>>>(c->partials, c->plane_sums, slot_stride(c), c->red_bx, c->g.nz, c->g.z0,
+                                             mask, cnt, cnt3, which, scalar_args(c, 0, 1), c->state, c->counter);
+    PN_CUDA(cudaGetLastError());
+    c->launches++;
+    return PN_OK;
 }
 
 int launch_scalar(pn_context *c, int which, int faithful, int blas_threads, cudaStream_t s) {
