@@ -592,6 +592,9 @@ static int group_apply(std::vector<pn_context *> &cs, int trans, int faithful, B
         for (auto *c : cs)
             PN_TRY(apply_planes(c, trans, faithful, (c->*in).p, (c->*out).p, red, jacobi, gated, s, seg, 0, -1));
     } else {
+        // the lazily assembled diagonal, before the exchange stream forks off
+        for (auto *c : cs)
+            if (faithful || !(c->canonical_diag && c->uniform_phase)) PN_TRY(ensure_diag(c, s));
         if (!c0->comm_stream) {
             PN_CUDA(cudaStreamCreateWithFlags(&c0->comm_stream, cudaStreamNonBlocking));
             PN_CUDA(cudaEventCreateWithFlags(&c0->cev_ready, cudaEventDisableTiming));
@@ -600,19 +603,21 @@ static int group_apply(std::vector<pn_context *> &cs, int trans, int faithful, B
         PN_CUDA(cudaEventRecord(c0->cev_ready, s));
         PN_CUDA(cudaStreamWaitEvent(c0->comm_stream, c0->cev_ready, 0));
         PN_TRY(halo_exchange(cs, in, c0->comm_stream));
-        PN_CUDA(cudaEventRecord(c0->cev_halo, c0->comm_stream));
         for (auto *c : cs) {
             const int nzl = c->g.nzl;
             if (nzl > 2)
                 PN_TRY(apply_planes(c, trans, faithful, (c->*in).p, (c->*out).p, red, jacobi, gated, s, seg, 1,
                                     nzl - 2));
         }
-        PN_CUDA(cudaStreamWaitEvent(s, c0->cev_halo, 0));
-        for (auto *c : cs) {   // planes 0 and nzl-1 in one launch
+        // planes 0 and nzl-1 in one launch on the exchange stream, right behind
+        // their halos: it runs beside the interior launch and fills its tail
+        for (auto *c : cs) {
             const int nzl = c->g.nzl;
-            PN_TRY(apply_planes(c, trans, faithful, (c->*in).p, (c->*out).p, red, jacobi, gated, s, seg, 0,
-                                nzl > 1 ? 2 : 1, nzl > 1 ? nzl - 1 : 1));
+            PN_TRY(apply_planes(c, trans, faithful, (c->*in).p, (c->*out).p, red, jacobi, gated, c0->comm_stream,
+                                seg, 0, nzl > 1 ? 2 : 1, nzl > 1 ? nzl - 1 : 1));
         }
+        PN_CUDA(cudaEventRecord(c0->cev_halo, c0->comm_stream));
+        PN_CUDA(cudaStreamWaitEvent(s, c0->cev_halo, 0));
     }
     if (!gather) return PN_OK;
     const int cnt = apply_red_count(c0, seg, faithful);
