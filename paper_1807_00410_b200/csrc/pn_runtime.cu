@@ -113,14 +113,19 @@ static int halo_exchange(std::vector<pn_context *> &cs, Buf pn_context::*vec, cu
 }
 
 // slots: bit mask of reduction slots every rank needs.  Block partials are
-// folded into per-plane sums locally; the plane sums are all-gathered.
-static int gather_partials(std::vector<pn_context *> &cs, int slots, cudaStream_t s, int nparts = -1) {
-    for (auto *c : cs) PN_TRY(launch_plane_sums(c, slots, nparts < 0 ? c->vec_bx : nparts, s));
+// folded into per-plane sums locally; the plane sums of `slots | also` are
+// all-gathered (`also`: slots whose plane sums an earlier call produced), the
+// NCCL calls of one gather grouped into one launch.
+static int gather_partials(std::vector<pn_context *> &cs, int slots, cudaStream_t s, int nparts = -1, int also = 0) {
+    if (slots)
+        for (auto *c : cs) PN_TRY(launch_plane_sums(c, slots, nparts < 0 ? c->vec_bx : nparts, s));
     pn_context *c0 = cs[0];
     if (c0->world <= 1) return PN_OK;
     const long long nz = c0->g.nz, cnt = c0->g.nzl;
+    const int gather = slots | also;
+    if (c0->nccl) PN_NCCL(ncclGroupStart());
     for (int q = 0; q < RED_SLOTS; ++q) {
-        if (!(slots >> q & 1)) continue;
+        if (!(gather >> q & 1)) continue;
         if (c0->nccl) {
             double *base = c0->plane_sums + q * nz;
             PN_NCCL(ncclAllGather(base + c0->g.z0, base, cnt, ncclDouble, (ncclComm_t)c0->nccl, s));
@@ -134,6 +139,7 @@ static int gather_partials(std::vector<pn_context *> &cs, int slots, cudaStream_
                 }
         }
     }
+    if (c0->nccl) PN_NCCL(ncclGroupEnd());
     return PN_OK;
 }
 
@@ -676,12 +682,16 @@ static int iteration(std::vector<pn_context *> &cs, const pn_solve_opts *o, bool
         PN_TRY(group_vec(cs, V_AXPY_ALPHA, &pn_context::x, &pn_context::p, nullptr, true, s));
         PN_TRY(group_vec(cs, V_AXMY_ALPHA, &pn_context::r, &pn_context::w, nullptr, true, s));
     } else {
-        // r -= alpha w (+ ||r||^2); x += alpha p is fused into the p update below
-        for (auto *c : cs) PN_TRY(launch_r_update(c, s));
-        PN_TRY(gather_partials(cs, 8, s));
+        // r -= alpha w (+ ||r||^2); x += alpha p is fused into the p update below.
+        // The ||r||^2 plane sums travel with the z reductions' exchange.
+        for (auto *c : cs) {
+            PN_TRY(launch_r_update(c, s));
+            PN_TRY(launch_plane_sums(c, 8, c->vec_bx, s));
+        }
     }
     // z = A^T r ; zt = z * minv ; rho' = z.zt ; ||z||, ||r||
-    PN_TRY(group_apply(cs, 1, F, &pn_context::r, &pn_context::z, F ? 0 : 2, jacobi, true, s, seg));
+    PN_TRY(group_apply(cs, 1, F, &pn_context::r, &pn_context::z, F ? 0 : 2, jacobi, true, s, seg, F != 0));
+    if (!F) PN_TRY(gather_partials(cs, 2 | 4, s, apply_red_count(cs[0], seg, 0), 8));
     if (F) {
         if (jacobi) PN_TRY(group_vec(cs, V_MUL, &pn_context::zt, &pn_context::z, &pn_context::minv, true, s));
         PN_TRY(group_dot(cs, &pn_context::z, ZT, 2, F, o, true, s));
