@@ -12,10 +12,13 @@ __host__ __device__ constexpr int seg_rows(int) { return PN_SEG_ROWS_OVERRIDE; }
 __host__ __device__ constexpr int seg_minb(int) { return PN_SEG_MINB_OVERRIDE; }
 __host__ __device__ constexpr bool seg_pair(int) { return PN_SEG_PAIR_OVERRIDE; }
 #else
-// pair: two warps share one staged row, each computing half of the classes
-__host__ __device__ constexpr bool seg_pair(int N) { return N >= 3; }
+// pair: two warps share one staged row, each computing half of the classes.
+// P5 (config 3): one warp per row, 4 CTAs of 4 rows per SM at 128 registers
+// (no spills) measured 328 vs 322 Gunk/s for warp pairs at 80 registers
+// (profiles/r01_sweep_p5_shape.log); P7 cannot hold 4 CTAs of staged rows.
+__host__ __device__ constexpr bool seg_pair(int N) { return N >= 3 && N != 5; }
 __host__ __device__ constexpr int seg_rows(int N) { return N <= 2 ? 8 : 4; }
-__host__ __device__ constexpr int seg_minb(int N) { return N <= 2 ? 4 : (N <= 6 ? 3 : 2); }
+__host__ __device__ constexpr int seg_minb(int N) { return N <= 2 ? 4 : (N == 5 ? 4 : (N <= 6 ? 3 : 2)); }
 #endif
 
 struct SegParams {
