@@ -16,6 +16,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <type_traits>
 
 #include "pn_internal.cuh"
@@ -231,16 +232,18 @@ struct SegItem {
 };
 
 template <int N>
-__device__ __forceinline__ SegItem seg_item(const SegGeo &g, long long vb, int rw) {
+__device__ __forceinline__ SegItem seg_item(const SegGeo &g, unsigned vb, int rw) {
     constexpr long long rowlen = (long long)(N + 1) * (N + 1) * 32;
     SegItem it;
-    it.seg = (int)(vb % g.nseg);
-    vb /= g.nseg;
-    const int tyb = min(g.tyb, g.nyb);
-    const int jb_in = (int)(vb % tyb);
-    vb /= tyb;
-    it.kl = g.kl0 + (int)(vb % g.npl) * g.kst;
-    it.jb = (int)(vb / g.npl) * tyb + jb_in;
+    unsigned q = fdiv(vb, g.dseg);
+    it.seg = (int)(vb - q * g.dseg.d);
+    vb = q;
+    q = fdiv(vb, g.dtyb);
+    const int jb_in = (int)(vb - q * g.dtyb.d);
+    vb = q;
+    q = fdiv(vb, g.dnpl);
+    it.kl = g.kl0 + (int)(vb - q * g.dnpl.d) * g.kst;
+    it.jb = (int)q * (int)g.dtyb.d + jb_in;
     it.j = it.jb < g.nyb ? it.jb * SegTune<N>::rows + rw : g.ny;
     it.kg = g.z0 + it.kl;
     it.rowbase = (((long long)it.kl * g.ny + it.j) * g.nseg + it.seg) * rowlen;
@@ -360,13 +363,14 @@ __device__ __forceinline__ void seg_partial(const SegGeo &g, const SegItem &it, 
                                             double *partials, long long slot_stride, int rb) {
     if (!RED) return;
     constexpr int W = SegTune<N>::rows * SegTune<N>::wpr;
-    double v0 = ra.s0, v1 = ra.s1, v2 = (RED == 2 && !JAC) ? ra.s1 : ra.s2;
+    double v0 = ra.s0, v1 = ra.s1, v2 = ra.s2;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        v0 += __shfl_down_sync(0xffffffffu, v0, o);
-        v1 += __shfl_down_sync(0xffffffffu, v1, o);
-        v2 += __shfl_down_sync(0xffffffffu, v2, o);
+    for (int o = 16; o > 0; o >>= 1) {   // only the sums this reduction writes
+        if (RED == 1) v0 += __shfl_down_sync(0xffffffffu, v0, o);
+        if (RED == 2) v1 += __shfl_down_sync(0xffffffffu, v1, o);
+        if (RED == 2 && JAC) v2 += __shfl_down_sync(0xffffffffu, v2, o);
     }
+    if (RED == 2 && !JAC) v2 = v1;
     if (lane == 0 && it.jb < g.nyb) {
         const long long idx = (long long)it.kg * rb + ((long long)it.seg * g.nyb + it.jb) * W + warp;
         if (RED == 1) partials[idx] = v0;
@@ -438,12 +442,18 @@ __global__ void PN_SEG_BOUNDS(N) k_seg(
 }
 
 template <int N>
-int seg_launch(const SegParams &prm, const SegGeo &g, int trans, int red, bool jac, const double *x, double *y,
+int seg_launch(const SegParams &prm, const SegGeo &g0, int trans, int red, bool jac, const double *x, double *y,
                const double *minv, double *zt, const double *st, const double *ss, double *partials,
                long long slot_stride, int rb, const State *state, cudaStream_t s) {
     constexpr int rows = SegTune<N>::rows;
+    SegGeo g = g0;
     const long long ytiles = (g.nyb + g.tyb - 1) / g.tyb;
-    dim3 grid((unsigned)((long long)g.nseg * g.tyb * g.npl * ytiles)), block(SegTune<N>::threads);
+    const long long nblk = (long long)g.nseg * g.tyb * g.npl * ytiles;
+    if (nblk >= (1LL << 31) - PN_SEG_PF) { set_error("segmented launch: grid too large"); return PN_ERR_INVALID; }
+    g.dseg = make_fastdiv((unsigned)g.nseg);
+    g.dtyb = make_fastdiv((unsigned)std::min(g.tyb, g.nyb));
+    g.dnpl = make_fastdiv((unsigned)g.npl);
+    dim3 grid((unsigned)nblk), block(SegTune<N>::threads);
     const size_t smem = rows * seg_smem_per_warp<N>();
     if (g.nyb != (g.ny + rows - 1) / rows) { set_error("segmented launch: row blocking mismatch"); return PN_ERR_INVALID; }
 #define PN_SEG_GO2(T, R, J, B)                                                                                  \

@@ -26,12 +26,32 @@ struct SegParams {
     double lamp[64];      // lambda_l * p_l per comp
 };
 
+// n / d for 0 <= n < 2^31 by multiply-high and shift (m = ceil(2^(31+l) / d),
+// l = ceil(log2 d)); d = 1 passes n through.  Replaces the 64-bit division
+// of the CTA -> row-block map (about 40 instructions each, three per CTA).
+struct FastDiv {
+    unsigned d, m, s;
+};
+inline FastDiv make_fastdiv(unsigned d) {
+    FastDiv f{d, 0u, 0u};
+    if (d <= 1) return f;
+    unsigned l = 0;
+    while ((1ull << l) < d) ++l;
+    f.m = (unsigned)(((1ull << (31 + l)) + d - 1) / d);
+    f.s = l - 1;
+    return f;
+}
+#ifdef __CUDACC__
+__device__ __forceinline__ unsigned fdiv(unsigned n, const FastDiv &f) { return f.m ? (__umulhi(n, f.m) >> f.s) : n; }
+#endif
+
 struct SegGeo {
     int U, nx, ny, nz, z0, nzl, nseg, nyb;
     int tyb;                 // row blocks per y-tile of the CTA traversal
     int kl0, npl, kst;       // local planes kl0 + i*kst, i < npl, computed by one launch
     int bulk;                // 1: bulk (TMA) staging path, for slabs far larger than L2
     long long plane, pvox;
+    FastDiv dseg, dtyb, dnpl;   // set per launch by seg_launch (nseg, min(tyb, nyb), npl)
 };
 
 struct State;
