@@ -95,6 +95,72 @@ __global__ void __launch_bounds__(256) k_csr_apply(long long n, const long long 
     }
 }
 
+// Fast-mode CSR product: CSR_SUB lanes per row, each striding the row's
+// entries by CSR_SUB (a lane group reads consecutive entries: full 32 B
+// sectors), partial sums folded by xor shuffles.  Row sums differ from the
+// stored-order sum only by rounding (fast mode); the faithful product keeps
+// one thread per row in stored order (k_csr_apply<true>).
+#ifndef PN_CSR_SUB
+#define PN_CSR_SUB 2
+#endif
+constexpr int CSR_SUB = PN_CSR_SUB;
+
+__global__ void __launch_bounds__(256) k_csr_apply_sub(long long n, const long long *__restrict__ p,
+                                                       const int *__restrict__ j, const double *__restrict__ a,
+                                                       const double *__restrict__ x, double *__restrict__ y, int red,
+                                                       const double *minv, double *zt, double *partials,
+                                                       long long slot_stride, int rb, const State *st) {
+    if (st && *(volatile const int *)&st->done) return;
+    const int lane = threadIdx.x & 31, sub = lane % CSR_SUB;
+    const int ngrp = blockDim.x / CSR_SUB;
+    const long long chunk = (n + rb - 1) / rb;
+    const long long r0 = (long long)blockIdx.x * chunk;
+    const long long r1 = min(n, r0 + chunk);
+    const long long wbase = r0 + (threadIdx.x >> 5) * (32 / CSR_SUB);
+    double acc0 = 0.0, acc1 = 0.0;
+    for (long long rb0 = wbase; rb0 < r1; rb0 += ngrp) {   // warp-uniform trip count
+        const long long r = rb0 + (lane / CSR_SUB);
+        const bool has = r < r1;
+        double sum = 0.0;
+        if (has) {
+            const long long ee = p[r + 1];
+#pragma unroll 2
+            for (long long e = p[r] + sub; e < ee; e += CSR_SUB) sum = fma(a[e], __ldg(x + j[e]), sum);
+        }
+#pragma unroll
+        for (int o = CSR_SUB / 2; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        if (has && sub == 0) {
+            y[r] = sum;
+            if (red == 1) acc0 = fma(sum, sum, acc0);
+            if (red == 2) {
+                const double t = minv ? sum * minv[r] : sum;
+                if (zt) zt[r] = t;
+                acc0 = fma(sum, t, acc0);
+                acc1 = fma(sum, sum, acc1);
+            }
+        }
+    }
+    if (!red) return;
+    __shared__ double sh[2][256];
+    sh[0][threadIdx.x] = acc0;
+    sh[1][threadIdx.x] = acc1;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if (threadIdx.x < o) {
+            sh[0][threadIdx.x] = __dadd_rn(sh[0][threadIdx.x], sh[0][threadIdx.x + o]);
+            sh[1][threadIdx.x] = __dadd_rn(sh[1][threadIdx.x], sh[1][threadIdx.x + o]);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        if (red == 1) partials[blockIdx.x] = sh[0][0];
+        else {
+            partials[2 * slot_stride + blockIdx.x] = sh[0][0];
+            partials[1 * slot_stride + blockIdx.x] = sh[1][0];
+        }
+    }
+}
+
 int csr_build(pn_context *c, long long n, long long nnz, const long long *h_ap, const int *h_aj, const double *h_ax) {
     CsrOp &o = c->csr;
     o.n = n;
@@ -399,9 +465,12 @@ int launch_csr_apply(pn_context *c, int trans, int faithful, int squared, const 
     if (faithful)
         k_csr_apply<true><<<c->vec_bx, 256, 0, s>>>(o.n, p, j, a, squared, x, y, red, minv, zt, c->partials, stride,
                                                     c->red_bx, st);
-    else
+    else if (squared)
         k_csr_apply<false><<<c->vec_bx, 256, 0, s>>>(o.n, p, j, a, squared, x, y, red, minv, zt, c->partials, stride,
                                                      c->red_bx, st);
+    else
+        k_csr_apply_sub<<<c->vec_bx, 256, 0, s>>>(o.n, p, j, a, x, y, red, minv, zt, c->partials, stride, c->red_bx,
+                                                  st);
     PN_CUDA(cudaGetLastError());
     c->launches++;
     return PN_OK;
