@@ -222,12 +222,10 @@ def run_ours(args):
     if world > 1:
         buf = [None]
         if rank == 0:
-            idb = bytearray(128)
             L = _lib.load()
-            cbuf = (np.zeros(128, np.uint8))
+            cbuf = np.zeros(128, np.uint8)
             _lib.check(L.pn_nccl_unique_id(cbuf.ctypes.data))
             buf[0] = bytes(cbuf)
-            del idb
         dist.broadcast_object_list(buf, src=0)
         nccl_id = buf[0]
     ctx = PnContext(tables, spec.res, spec.h, device=local, z0=z0, nz_local=nzl, rank=rank, world=world,
@@ -286,7 +284,6 @@ def run_ours(args):
     # with the sigma_t floor tau = 1 its vacuum needs, configs.solve_spec)
     ttr = None
     if rank == 0 and not args.skip_ttr:
-        from paper_1807_00410_b200.configs import solve_spec
         ttr = {}
         for idx, ref_it in ((2, 259), (3, None)):
             co = make_config(idx)

@@ -12,7 +12,6 @@ against committed fixtures generated from it (tests/golden/, tools/make_goldens.
 from __future__ import annotations
 
 import ctypes
-import os
 import pathlib
 import subprocess
 
