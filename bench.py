@@ -262,6 +262,10 @@ def run_ours(args):
                 "algorithmic_bytes_per_launch": bytes_apply,
                 "bytes_formula": "8*nvox*(2U+2): read u, write A u, read sigma_t and sigma_s"}
 
+    # algorithmic bytes of one fused iteration (per GPU): two applies, r -= alpha w
+    # (read r, w; write r) and x += alpha p; p = z + beta p (read x, p, z; write x, p)
+    it_bytes = 2 * bytes_apply + 8 * 8 * nvox_l * U
+
     # ---- the other single-GPU configurations' apply throughput (rank 0, context)
     others = None
     if rank == 0 and not args.skip_others:
@@ -350,6 +354,10 @@ def run_ours(args):
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
             "cg_iteration": {"ms": ms_iter, "gunk_s_2_applies": 2 * R / (ms_iter / 1e3) / 1e9,
+                             "algorithmic_bytes": it_bytes, "achieved_gbs": it_bytes / (ms_iter / 1e3) / 1e9,
+                             "frac": it_bytes / (ms_iter / 1e3) / 1e9 / peak,
+                             "bytes_formula": "2 applies + 8 vector passes of 8R bytes (r -= alpha w: 3, "
+                                              "x += alpha p; p = z + beta p: 5), per GPU",
                              "what": "one fused CGNR iteration: A p + ww, alpha, x/r update + rr, A^T r + zz/zzt, "
                                      "beta, p update"},
             "time_to_residual": ttr,
