@@ -277,7 +277,11 @@ class PnContext:
         o.primal_tol = -1.0 if primal_tol is None else float(primal_tol)
         o.jacobi = int(bool(jacobi))
         o.mode = 1 if mode == "faithful" else 0
-        th, kn = blas_config()
+        # the OpenBLAS configuration matters to the faithful mode only (its ddot
+        # emulation); querying it scans the loaded libraries (~0.5 ms per call)
+        th, kn = (8, 0)
+        if o.mode == 1 and (blas_threads is None or blas_kernel is None):
+            th, kn = blas_config()
         o.blas_threads = int(blas_threads if blas_threads is not None else th)
         o.blas_kernel = int(blas_kernel if blas_kernel is not None else kn)
         o.check_every = int(check_every)
