@@ -237,6 +237,37 @@ def test_csr_nonconvergence_and_jacobi():
     np.testing.assert_allclose(x0, x1, atol=1e-6)
 
 
+@pytest.mark.parametrize("n", [1, 37, 3001])
+def test_csr_products_ragged_rows(n):
+    """Generic CSR with empty rows, single entries and long rows (up to 300
+    entries, odd and even lengths): the fast product (two lanes per row,
+    shuffle fold) within rounding of scipy, the faithful product (one thread
+    per row, stored order, mul-then-add) bit-identical to scipy's csr_matvec,
+    for A and A^T."""
+    import scipy.sparse as sp
+    import torch
+    from paper_1807_00410_b200.solver import PnContext
+    rng = np.random.default_rng(n)
+    lens = rng.choice([0, 1, 2, 3, 7, 10, 33, 300], size=n, p=[.15, .15, .1, .1, .2, .2, .05, .05])
+    rows, cols = [], []
+    for i, L in enumerate(lens):
+        c = np.sort(rng.choice(n, size=min(int(L), n), replace=False))
+        rows += [i] * len(c)
+        cols += list(c)
+    A = sp.csr_matrix((rng.normal(size=len(rows)), (rows, cols)), shape=(n, n))
+    A.sort_indices()
+    x = rng.normal(size=n)
+    c = PnContext.from_csr(A)
+    for tr, M in ((False, A), (True, A.T.tocsr())):
+        want = M @ x
+        fast = c.apply(x, transpose=tr).cpu().numpy()
+        scale = abs(M) @ np.abs(x)
+        assert np.all(np.abs(fast - want) <= 1e-13 * scale)   # ~ 900 ulp of sum |a x|, rows up to 300
+        faithful = c.apply(x, transpose=tr, mode="faithful").cpu().numpy()
+        assert faithful.tobytes() == want.tobytes()
+    torch.cuda.synchronize()
+
+
 @pytest.mark.parametrize("case", ["p3_456", "p7_343", "p1_3286"])
 @pytest.mark.parametrize("jac", [0, 1])
 def test_csr_faithful_bit_identical_to_reference(case, jac, golden):
