@@ -118,13 +118,18 @@ def main():
     if "--cda-only" in sys.argv:
         cda()
         return
+    if "--tables-2d-only" in sys.argv:   # 2-D tables up to P5 (the paper's checkerboard runs)
+        for N in (1, 2, 3, 4, 5):
+            t = tables_from_program(compile_program(build_pn(N, 2)))
+            (GOLD / f"tables_N{N}_2d.json").write_text(json.dumps(to_json(t), separators=(",", ":")))
+        return
     neumann()
     cda()
     GOLD.mkdir(parents=True, exist_ok=True)
     for N in range(1, 8):
         t = tables_from_program(compile_program(build_pn(N, 3)))
         (GOLD / f"tables_N{N}.json").write_text(json.dumps(to_json(t), separators=(",", ":")))
-    for N in (1, 2, 3):
+    for N in (1, 2, 3, 4, 5):
         t = tables_from_program(compile_program(build_pn(N, 2)))
         (GOLD / f"tables_N{N}_2d.json").write_text(json.dumps(to_json(t), separators=(",", ":")))
     arrs = {}
