@@ -17,6 +17,7 @@
 #include <math.h>
 
 #include "pn_internal.cuh"
+#include "pn_seg_types.cuh"
 
 namespace pn {
 
@@ -204,7 +205,8 @@ __global__ void __launch_bounds__(256) k_apply_table(Tables T, Fields F, Geo g, 
                                                      const double *__restrict__ x, double *__restrict__ y,
                                                      const double *__restrict__ diag, int red, const double *minv,
                                                      double *zt, double *partials, long long slot_stride, int rb,
-                                                     const State *st, int kl0, int kst, int pst) {
+                                                     const State *st, int kl0, int kst, int pst, FastDiv du,
+                                                     FastDiv dnx) {
     if (st && stopped(st)) return;
     extern __shared__ unsigned char smem_raw[];
     const int U = g.U;
@@ -214,6 +216,7 @@ __global__ void __launch_bounds__(256) k_apply_table(Tables T, Fields F, Geo g, 
     int *soth = sptr + U + 1, *sdir = soth + ne, *sisd = sdir + ne;
     int *spar = sisd + ne;
     double *slamp = (double *)(((uintptr_t)(spar + U) + 15) & ~(uintptr_t)15);
+    int *sdg = (int *)(slamp + U);   // fast path: the diagonal entry of each row, -1 if none
     {
         const int *p_ = trans ? T.t_ptr : T.a_ptr;
         const int *o_ = trans ? T.t_src : T.a_tgt;
@@ -225,6 +228,12 @@ __global__ void __launch_bounds__(256) k_apply_table(Tables T, Fields F, Geo g, 
         }
         for (int e = threadIdx.x; e <= U; e += blockDim.x) sptr[e] = p_[e];
         for (int e = threadIdx.x; e < U; e += blockDim.x) { spar[e] = T.par[e]; slamp[e] = T.lamp[e]; }
+        for (int cc = threadIdx.x; cc < U; cc += blockDim.x) {
+            int dg = -1;
+            for (int e = p_[cc]; e < p_[cc + 1]; ++e)
+                if (i_[e]) dg = e;
+            sdg[cc] = dg;
+        }
     }
     __syncthreads();
     const int kl = kl0 + blockIdx.y * kst;
@@ -235,16 +244,40 @@ __global__ void __launch_bounds__(256) k_apply_table(Tables T, Fields F, Geo g, 
     const int kg = g.z0 + kl;
     for (long long rp = r0 + threadIdx.x; rp < r1; rp += blockDim.x) {
         const long long row = (long long)kl * g.plane + rp;
-        const long long vp = rp / U;
-        const int c = (int)(rp - vp * U);
-        const int i = (int)(vp % g.nx), j = (int)(vp / g.nx);
+        // (voxel, comp) and (i, j) by multiply-high division (plane < 2^31, checked at launch)
+        const unsigned vp = fdiv((unsigned)rp, du);
+        const int c = (int)((unsigned)rp - vp * (unsigned)U);
+        const unsigned jq = fdiv(vp, dnx);
+        const int i = (int)(vp - jq * (unsigned)g.nx), j = (int)jq;
         const int bb = boundary_bits(g, i, j, kg);
         const bool pinned_c = (spar[c] & bb) != 0;
         double sum = 0.0;
+        if (!FAITHFUL && sdg[c] >= 0) {
+            // fast: the diagonal term once per row, ahead of the (lane-divergent)
+            // entry loop, instead of whenever some lane of the warp reaches it
+            double a;
+            if (RECOMPUTE_DIAG) {
+                const int pc = spar[c];
+                double st_ = 0.0, ss_ = 0.0;
+                int n = 0;
+                for (int s = 0; s < 8; ++s) {
+                    if (s & ~pc) continue;
+                    st_ += fsample(F, g, 0, i, j, kl, s);
+                    ss_ += fsample(F, g, 1, i, j, kl, s);
+                    ++n;
+                }
+                const double inv = 1.0 / n;
+                a = st_ * inv - slamp[c] * (ss_ * inv);
+            } else {
+                a = diag[row];
+            }
+            sum = a * x[row];
+        }
         for (int e = sptr[c]; e < sptr[c + 1]; ++e) {
             const int o = soth[e];
             double a, xv;
             if (sisd[e]) {
+                if (!FAITHFUL) continue;   // done above
                 if (RECOMPUTE_DIAG) {
                     // avg over the staggered site set, then diag = avg_t - lamp*avg_s
                     const int pc = spar[c];
@@ -306,7 +339,7 @@ static size_t table_smem(const pn_context *c, int trans) {
     int ne = trans ? c->tb.n_t : c->tb.n_a;
     size_t b = (size_t)ne * 8 + (size_t)(c->U + 1) * 4 + (size_t)ne * 12 + (size_t)c->U * 4;
     b = (b + 15) & ~(size_t)15;
-    return b + (size_t)c->U * 8 + 16;
+    return b + (size_t)c->U * 8 + (size_t)c->U * 4 + 16;
 }
 
 static long long slot_stride(const pn_context *c) { return (long long)c->g.nz * c->red_bx; }
@@ -320,15 +353,17 @@ int launch_apply_table(pn_context *c, int trans, int faithful, int squared, cons
     const State *st = gated ? c->state : nullptr;
     bool recompute = !faithful && c->canonical_diag && c->uniform_phase;
     if (!recompute && !c->diag_ready) { set_error("internal: diagonal not assembled"); return PN_ERR_INVALID; }
+    if (c->g.plane >= (1LL << 31)) { set_error("table operator: z-plane too large"); return PN_ERR_UNSUPPORTED; }
+    const FastDiv du = make_fastdiv((unsigned)c->U), dnx = make_fastdiv((unsigned)c->g.nx);
     if (faithful) {
         k_apply_table<true, false><<<grid, 256, sm, s>>>(c->tb, c->f, c->g, trans, squared, x, y, c->diag, red, minv,
-                                                         zt, c->partials, slot_stride(c), c->vec_bx, st, kl0, kst, c->red_bx);
+                                                         zt, c->partials, slot_stride(c), c->vec_bx, st, kl0, kst, c->red_bx, du, dnx);
     } else if (recompute) {
         k_apply_table<false, true><<<grid, 256, sm, s>>>(c->tb, c->f, c->g, trans, 0, x, y, c->diag, red, minv, zt,
-                                                         c->partials, slot_stride(c), c->vec_bx, st, kl0, kst, c->red_bx);
+                                                         c->partials, slot_stride(c), c->vec_bx, st, kl0, kst, c->red_bx, du, dnx);
     } else {
         k_apply_table<false, false><<<grid, 256, sm, s>>>(c->tb, c->f, c->g, trans, 0, x, y, c->diag, red, minv, zt,
-                                                          c->partials, slot_stride(c), c->vec_bx, st, kl0, kst, c->red_bx);
+                                                          c->partials, slot_stride(c), c->vec_bx, st, kl0, kst, c->red_bx, du, dnx);
     }
     PN_CUDA(cudaGetLastError());
     c->launches++;
