@@ -182,6 +182,13 @@ struct pn_context {
     pn::CsrOp csr;
 
     long long R_l() const { return (long long)g.nzl * g.plane; }
+    // solve layout of the segmented operator: rows of 32 voxels along x, the
+    // last one zero-padded when nx % 32 != 0 (single-slab contexts only);
+    // splane doubles per z-plane (== g.plane without padding)
+    long long splane = 0;
+    bool seg_active = false;      // a fast segmented solve / bench is running: vector kernels use splane
+    long long R_s() const { return (long long)g.nzl * splane; }
+    long long vplane() const { return seg_active ? splane : g.plane; }
     long long nvox_l() const { return (long long)g.nzl * g.pvox; }
 };
 

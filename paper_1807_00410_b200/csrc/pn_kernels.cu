@@ -376,6 +376,15 @@ int launch_apply_faithful(pn_context *c, int trans, int squared, const double *x
 }
 
 // ----------------------------------------------------------- vector ops --
+// geometry of the vectors the current operation works on: the segmented solve
+// layout (x padded to whole rows) during fast segmented solves, else the
+// reference layout
+static Geo vgeo(const pn_context *c) {
+    Geo g = c->g;
+    g.plane = c->vplane();
+    return g;
+}
+
 __global__ void __launch_bounds__(256) k_vec(int op, Geo g, double *y, const double *a, const double *b, State *st,
                                              double *partials, long long slot_stride, int rb, int gated) {
     if (gated && stopped(st)) return;
@@ -530,7 +539,7 @@ __global__ void __launch_bounds__(256) k_dot(Geo g, const double *__restrict__ a
 
 int launch_vec(pn_context *c, int op, double *y, const double *a, const double *b, cudaStream_t s, bool gated) {
     dim3 grid(c->vec_bx, c->g.nzl);
-    k_vec<<<grid, 256, 0, s>>>(op, c->g, y, a, b, c->state, c->partials, slot_stride(c), c->vec_bx, gated ? 1 : 0);
+    k_vec<<<grid, 256, 0, s>>>(op, vgeo(c), y, a, b, c->state, c->partials, slot_stride(c), c->vec_bx, gated ? 1 : 0);
     PN_CUDA(cudaGetLastError());
     c->launches++;
     return PN_OK;
@@ -538,7 +547,7 @@ int launch_vec(pn_context *c, int op, double *y, const double *a, const double *
 
 int launch_r_update(pn_context *c, cudaStream_t s) {
     dim3 grid(c->vec_bx, c->g.nzl);
-    k_r<<<grid, 256, 0, s>>>(c->g, c->r.p, c->w.p, c->state, c->partials, slot_stride(c), c->vec_bx, c->red_bx);
+    k_r<<<grid, 256, 0, s>>>(vgeo(c), c->r.p, c->w.p, c->state, c->partials, slot_stride(c), c->vec_bx, c->red_bx);
     PN_CUDA(cudaGetLastError());
     c->launches++;
     return PN_OK;
@@ -546,7 +555,7 @@ int launch_r_update(pn_context *c, cudaStream_t s) {
 
 int launch_xp_update(pn_context *c, const double *zt, cudaStream_t s) {
     dim3 grid(c->vec_bx, c->g.nzl);
-    k_xp<<<grid, 256, 0, s>>>(c->g, c->x.p, c->p.p, zt, c->state, c->vec_bx);
+    k_xp<<<grid, 256, 0, s>>>(vgeo(c), c->x.p, c->p.p, zt, c->state, c->vec_bx);
     PN_CUDA(cudaGetLastError());
     c->launches++;
     return PN_OK;
@@ -554,7 +563,7 @@ int launch_xp_update(pn_context *c, const double *zt, cudaStream_t s) {
 
 int launch_dot(pn_context *c, const double *a, const double *b, int slot, cudaStream_t s, bool gated) {
     dim3 grid(c->vec_bx, c->g.nzl);
-    k_dot<<<grid, 256, 0, s>>>(c->g, a, b, slot, c->partials, slot_stride(c), c->vec_bx, gated ? c->state : nullptr,
+    k_dot<<<grid, 256, 0, s>>>(vgeo(c), a, b, slot, c->partials, slot_stride(c), c->vec_bx, gated ? c->state : nullptr,
                                c->red_bx);
     PN_CUDA(cudaGetLastError());
     c->launches++;

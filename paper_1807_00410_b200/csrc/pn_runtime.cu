@@ -66,12 +66,26 @@ static int dcopy(pn_context *c, T **dst, const T *src, size_t n) {
 
 static int alloc_buf(pn_context *c, Buf &b) {
     if (b.alloc) return PN_OK;
-    size_t n = (size_t)(c->g.nzl + 2) * c->g.plane;
+    // room for either layout; the halo planes (multi-slab only) are g.plane
+    // wide there, and the interior base stays 256 B aligned in both
+    const long long pl = std::max(c->g.plane, c->splane ? c->splane : c->g.plane);
+    size_t n = (size_t)(c->g.nzl + 2) * pl;
     PN_TRY(dalloc(c, &b.alloc, n));
     PN_CUDA(cudaMemset(b.alloc, 0, n * sizeof(double)));
-    b.p = b.alloc + c->g.plane;
+    b.p = b.alloc + pl;
     return PN_OK;
 }
+
+// marks a fast segmented solve / product: vector kernels run over the solve layout
+struct SegActive {
+    std::vector<pn_context *> &cs;
+    SegActive(std::vector<pn_context *> &cs_, bool on) : cs(cs_) {
+        for (auto *c : cs) c->seg_active = on;
+    }
+    ~SegActive() {
+        for (auto *c : cs) c->seg_active = false;
+    }
+};
 
 static int ensure_diag(pn_context *c, cudaStream_t s) {
     if (c->diag_ready) return PN_OK;
@@ -189,6 +203,11 @@ int pn_create(const pn_desc *d, pn_context **out) {
     g.U = d->U; g.nx = d->nx; g.ny = d->ny; g.nz = d->nz; g.z0 = d->z0; g.nzl = d->nz_local;
     g.pvox = (long long)d->nx * d->ny;
     g.plane = g.pvox * d->U;
+    // segmented solve layout: x padded to whole 32-voxel rows on single-slab
+    // contexts (multi-slab decompositions keep nx % 32 == 0 for the fast path)
+    bool pad = d->nx % 32 != 0 && c->world <= 1;
+    if (const char *e = getenv("PNRTE_SEG_PAD")) pad = pad && atoi(e) != 0;   // 0: table operator instead
+    c->splane = pad ? (long long)d->ny * ((d->nx + 31) / 32) * 32 * d->U : g.plane;
     c->h_par.assign(d->par, d->par + d->U);
     c->h_lam.assign(d->lam, d->lam + d->U);
     c->h_lidx.assign(d->lidx, d->lidx + d->U);
@@ -777,6 +796,7 @@ static int solve_group(std::vector<pn_context *> &cs, const pn_solve_opts *o, co
     const bool jacobi = o->jacobi != 0;
     bool seg = !F;
     for (auto *c : cs) seg = seg && pn_seg_ok(c);
+    SegActive seg_active(cs, seg);
     for (auto *c : cs) {
         PN_CUDA(cudaSetDevice(c->device));
         if (!c->setup_done) { set_error("pn_setup not called"); return PN_ERR_INVALID; }
@@ -818,16 +838,18 @@ static int solve_group(std::vector<pn_context *> &cs, const pn_solve_opts *o, co
     }
     if (jacobi) {
         // minv = 1 / colsum(A o A), 0 -> 1 (solver.py:218-223), exact order, then solve layout
+        for (auto *c : cs) c->seg_active = false;   // reference-layout vectors here
         PN_TRY(group_vec(cs, V_FILL_ONE, &pn_context::tmp, nullptr, nullptr, false, s));
         PN_TRY(halo_exchange(cs, &pn_context::tmp, s));
         for (auto *c : cs) PN_TRY(squared_transpose_apply(c, c->tmp.p, c->w.p, s));
         PN_TRY(group_vec(cs, V_RECIP_DIAG, &pn_context::tmp, &pn_context::w, nullptr, false, s));
+        for (auto *c : cs) c->seg_active = seg;
         for (auto *c : cs) PN_TRY(to_solve_layout(c, seg, c->tmp.p, c->minv.p, s));
     }
     // x = x0 ; r = b - A x ; z = A^T r ; zt ; p = zt ; rho = z.zt
     for (size_t i = 0; i < cs.size(); ++i) {
         if (x0s && x0s[i]) PN_TRY(to_solve_layout(cs[i], seg, x0s[i], cs[i]->x.p, s));
-        else PN_CUDA(cudaMemsetAsync(cs[i]->x.p, 0, cs[i]->R_l() * sizeof(double), s));
+        else PN_CUDA(cudaMemsetAsync(cs[i]->x.p, 0, (seg ? cs[i]->R_s() : cs[i]->R_l()) * sizeof(double), s));
     }
     PN_TRY(group_apply(cs, 0, F, &pn_context::x, &pn_context::tmp, 0, false, false, s, seg));
     PN_TRY(group_vec(cs, V_SUB, &pn_context::r, &pn_context::bs, &pn_context::tmp, false, s));
@@ -988,6 +1010,7 @@ int pn_bench(pn_context *c, int32_t what, int32_t reps, double *ms_per, void *st
     PN_TRY(ensure_vectors(c, false));
     std::vector<pn_context *> cs{c};
     const bool seg = pn_seg_ok(c);
+    SegActive seg_active(cs, seg);
     cudaEvent_t e0, e1;
     PN_CUDA(cudaEventCreate(&e0));
     PN_CUDA(cudaEventCreate(&e1));

@@ -18,22 +18,38 @@ struct SegCtx {
     SegParams *pa = nullptr, *pt = nullptr;   // host parameter blocks (A, A^T)
     SegGeo g{};
     bool ok = false;
+    double *sig_pad = nullptr;                // padded sigma_t / sigma_s slabs (nx % 32 != 0)
+    size_t sig_pad_n = 0;                     // doubles per field
 };
 
+static bool seg_padded(const pn_context *c) { return c->g.nx % 32 != 0; }
+
 static bool seg_geometry_ok(const pn_context *c) {
-    return c->g.nx % 32 == 0 && c->N >= 1 && c->N <= 7 && c->canonical_diag && c->U <= 64;
+    // a partial last row is zero-padded in the solve layout (single-slab contexts)
+    return (c->g.nx % 32 == 0 || c->splane != c->g.plane) && c->N >= 1 && c->N <= 7 && c->canonical_diag &&
+           c->U <= 64;
 }
 
 int pn_seg_red_blocks(const pn_context *c) {
     if (!seg_geometry_ok(c)) return 0;
     // one reduction partial per warp: segments x row blocks x warps per CTA
     const int warps = seg_rows(c->N) * (seg_pair(c->N) ? 2 : 1);
-    return (c->g.nx / 32) * ((c->g.ny + seg_rows(c->N) - 1) / seg_rows(c->N)) * warps;
+    return ((c->g.nx + 31) / 32) * ((c->g.ny + seg_rows(c->N) - 1) / seg_rows(c->N)) * warps;
+}
+
+// sigma slab ((nzl+1) planes, rows of nx) -> rows of sx >= nx, edge-replicated in x
+__global__ void k_sig_pad(const double *__restrict__ src, double *__restrict__ dst, int nx, int sx, long long rows) {
+    const long long n = rows * sx;
+    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x) {
+        const long long row = t / sx;
+        const int i = (int)(t - row * sx);
+        dst[t] = src[row * nx + min(i, nx - 1)];
+    }
 }
 
 bool pn_seg_ok(const pn_context *c) { return c->seg && ((SegCtx *)c->seg)->ok; }
 
-int pn_seg_prepare(pn_context *c, cudaStream_t) {
+int pn_seg_prepare(pn_context *c, cudaStream_t s) {
     SegCtx *sc = (SegCtx *)c->seg;
     if (!sc) {
         sc = new SegCtx();
@@ -65,14 +81,29 @@ int pn_seg_prepare(pn_context *c, cudaStream_t) {
     for (int q = 0; q < c->U; ++q) sc->pa->lamp[q] = sc->pt->lamp[q] = lamp[q];
     SegGeo &g = sc->g;
     g.U = c->U; g.nx = c->g.nx; g.ny = c->g.ny; g.nz = c->g.nz; g.z0 = c->g.z0; g.nzl = c->g.nzl;
-    g.nseg = c->g.nx / 32;
+    g.nseg = (c->g.nx + 31) / 32;
+    g.sx = seg_padded(c) ? g.nseg * 32 : c->g.nx;
     g.nyb = (c->g.ny + seg_rows(c->N) - 1) / seg_rows(c->N);
     // planes above ~12 MB: march in z inside y-tiles of ~32 rows so the z
     // neighbour rows stay in L2; smaller planes: plain (x, y, z) order
     const double plane_mb = (double)c->g.plane * sizeof(double) / 1e6;
     g.tyb = plane_mb > 12.0 ? std::min(g.nyb, std::max(1, 32 / seg_rows(c->N))) : g.nyb;
-    g.plane = c->g.plane;
+    g.plane = c->splane;   // solve layout (== c->g.plane unless padded)
     g.pvox = c->g.pvox;
+    if (seg_padded(c)) {
+        const long long rows = (long long)(c->g.nzl + 1) * c->g.ny;
+        const size_t n = (size_t)rows * g.sx;
+        if (sc->sig_pad_n != n) {
+            if (sc->sig_pad) cudaFree(sc->sig_pad);
+            sc->sig_pad = nullptr;
+            PN_CUDA(cudaMalloc(&sc->sig_pad, 2 * n * sizeof(double)));
+            sc->sig_pad_n = n;
+        }
+        for (int f = 0; f < 2; ++f) {
+            k_sig_pad<<<1184, 256, 0, s>>>(c->f.data[f], sc->sig_pad + f * n, c->g.nx, g.sx, rows);
+            PN_CUDA(cudaGetLastError());
+        }
+    }
     // bulk (TMA) staging + in-CTA y neighbours where the vector streams from
     // HBM (measured +2-4 % at 128^3 and 256^3); cp.async where it sits in L2
     // (64^3: the bulk path measured ~10 % slower).  PNRTE_SEG_BULK=0/1 forces.
@@ -95,6 +126,10 @@ int pn_seg_apply(pn_context *c, int trans, const double *x, double *y, int red, 
     const long long stride = (long long)c->g.nz * c->red_bx;
     const State *st = gated ? c->state : nullptr;
     const double *sig_t = c->f.data[0], *sig_s = c->f.data[1];
+    if (sc->sig_pad) {
+        sig_t = sc->sig_pad;
+        sig_s = sc->sig_pad + sc->sig_pad_n;
+    }
     int rc;
     switch (c->N) {
 #define PN_N(n)                                                                                                 \
@@ -111,31 +146,50 @@ int pn_seg_apply(pn_context *c, int trans, const double *x, double *y, int red, 
 }
 
 // dir 0: reference layout (voxel-major, comp-minor) -> segmented; 1: back.
-__global__ void k_seg_convert(int dir, int U, const double *__restrict__ src, double *__restrict__ dst) {
+// One block per 32-voxel row; a partial last row (w < 32 voxels, nx % 32 != 0)
+// is zero-filled beyond w in the segmented layout and its padding is dropped
+// on the way back.
+__global__ void k_seg_convert(int dir, int U, int nx, int nseg, const double *__restrict__ src,
+                              double *__restrict__ dst) {
     extern __shared__ double tile[];   // 32 x (U+1)
-    const long long base = (long long)blockIdx.x * 32 * U;
+    const long long row = blockIdx.x;  // (kl, j) line * nseg + seg
+    const long long line = row / nseg;
+    const int seg = (int)(row - line * nseg);
+    const int w = min(32, nx - seg * 32);
+    const long long rbase = (line * nx + seg * 32) * U;   // reference layout
+    const long long sbase = row * 32 * U;                 // segmented layout
     const int n = 32 * U;
     for (int t = threadIdx.x; t < n; t += blockDim.x) {
-        double v = src[base + t];
         int l, c;
-        if (dir == 0) { l = t / U; c = t - l * U; }
-        else { c = t >> 5; l = t & 31; }
+        double v;
+        if (dir == 0) {
+            l = t / U; c = t - l * U;
+            v = l < w ? src[rbase + t] : 0.0;
+        } else {
+            c = t >> 5; l = t & 31;
+            v = src[sbase + t];
+        }
         tile[l * (U + 1) + c] = v;
     }
     __syncthreads();
     for (int t = threadIdx.x; t < n; t += blockDim.x) {
         int l, c;
-        if (dir == 0) { c = t >> 5; l = t & 31; }
-        else { l = t / U; c = t - l * U; }
-        dst[base + t] = tile[l * (U + 1) + c];
+        if (dir == 0) {
+            c = t >> 5; l = t & 31;
+            dst[sbase + t] = tile[l * (U + 1) + c];
+        } else {
+            l = t / U; c = t - l * U;
+            if (l < w) dst[rbase + t] = tile[l * (U + 1) + c];
+        }
     }
 }
 
 int pn_seg_convert(pn_context *c, int dir, const double *src, double *dst, cudaStream_t s) {
     if (src == dst) { set_error("pn_seg_convert: in-place"); return PN_ERR_INVALID; }
-    long long rows = (long long)c->g.nzl * c->g.ny * (c->g.nx / 32);
+    const int nseg = (c->g.nx + 31) / 32;
+    long long rows = (long long)c->g.nzl * c->g.ny * nseg;
     size_t sm = (size_t)32 * (c->U + 1) * sizeof(double);
-    k_seg_convert<<<(unsigned)rows, 256, sm, s>>>(dir, c->U, src, dst);
+    k_seg_convert<<<(unsigned)rows, 256, sm, s>>>(dir, c->U, c->g.nx, nseg, src, dst);
     PN_CUDA(cudaGetLastError());
     c->launches++;
     return PN_OK;
@@ -146,6 +200,7 @@ void pn_seg_release(pn_context *c) {
     if (!sc) return;
     delete sc->pa;
     delete sc->pt;
+    if (sc->sig_pad) cudaFree(sc->sig_pad);
     delete sc;
     c->seg = nullptr;
 }

@@ -36,6 +36,7 @@ struct SegRow {
     const double *diag;                     // stored diagonal row + lane (DIAG_ARRAY)
     int lane;
     bool bx, bx_p, by, bz, by_p, bz_p;      // last-face flags: own voxel, x+1, y+1 row, z+1 row
+    bool xpad;                              // lane beyond nx in a zero-padded last row (output 0)
     static constexpr bool ysm = false;      // y-neighbour rows always in global memory
 };
 // bulk path: a y-neighbour row may be a staged row of this CTA (shared memory)
@@ -280,7 +281,7 @@ __device__ __forceinline__ void seg_stage(const SegGeo &g, const SegItem &it, do
         const int rowq = q >> 4, part = (q & 15) * 2, fld = rowq >> 2, r4 = rowq & 3;
         const int jj = min(it.j + (r4 & 1), g.ny - 1);
         const int kk = it.kl + (r4 >> 1);   // plane nzl exists (edge-replicated at upload)
-        const long long vb = ((long long)kk * g.ny + jj) * g.nx + it.seg * 32;
+        const long long vb = ((long long)kk * g.ny + jj) * g.sx + it.seg * 32;
         cp_async16(sg + fld * 136 + r4 * 34 + part, (fld ? ss : st) + vb + part);
     }
     if (half == WPR - 1) {
@@ -288,7 +289,7 @@ __device__ __forceinline__ void seg_stage(const SegGeo &g, const SegItem &it, do
             const int fld = lane >> 2, r4 = lane & 3;
             const int jj = min(it.j + (r4 & 1), g.ny - 1);
             const int kk = it.kl + (r4 >> 1);
-            const long long vb = ((long long)kk * g.ny + jj) * g.nx + it.seg * 32 + (has_next ? 32 : 31);
+            const long long vb = ((long long)kk * g.ny + jj) * g.sx + it.seg * 32 + (has_next ? 32 : 31);
             cp_async8(sg + fld * 136 + r4 * 34 + 32, (fld ? ss : st) + vb);
         }
         for (int c = lane; c < U; c += 32) {
@@ -336,6 +337,7 @@ __device__ __forceinline__ void seg_compute(const SegParams &prm, const SegGeo &
     r.minv = minv ? minv + it.rowbase + lane : nullptr;
     r.zt = zt ? zt + it.rowbase + lane : nullptr;
     r.diag = nullptr;
+    r.xpad = i >= g.nx;
     r.bx = i == g.nx - 1;
     r.bx_p = i + 1 == g.nx - 1;
     r.by = it.j == g.ny - 1;

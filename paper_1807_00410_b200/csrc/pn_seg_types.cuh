@@ -49,6 +49,7 @@ struct SegGeo {
     int U, nx, ny, nz, z0, nzl, nseg, nyb;
     int tyb;                 // row blocks per y-tile of the CTA traversal
     int kl0, npl, kst;       // local planes kl0 + i*kst, i < npl, computed by one launch
+    int sx;                  // row stride of the sigma slabs the kernel reads (nx, or nseg*32 when padded)
     int bulk;                // 1: bulk (TMA) staging path, for slabs far larger than L2
     long long plane, pvox;
     FastDiv dseg, dtyb, dnpl;   // set per launch by seg_launch (nseg, min(tyb, nyb), npl)

@@ -12,6 +12,11 @@ from paper_1807_00410_b200.configs import make_config, solve_spec
 from paper_1807_00410_b200.problems import ProblemSpec, phase_fields
 from paper_1807_00410_b200.program import build_tables, q_name
 
+
+def rel(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
 pytestmark = pytest.mark.gpu
 
 
@@ -156,9 +161,12 @@ def test_loopback_slabs_match_single_slab(N, res, slabs, bulk, monkeypatch):
     the single-GPU result bit for bit, for the operator and the full solve;
     with the segmented kernel's cp.async (bulk=0) and bulk/TMA (bulk=1)
     staging paths (the plane-range launches of the interior / boundary planes
-    differ between the two)."""
+    differ between the two).  Grids with nx % 32 != 0 run the table operator
+    on slabs, so the single context is pinned to it too (PNRTE_SEG_PAD=0; the
+    zero-padded segmented path is checked in test_padded_segmented_path)."""
     import torch
     monkeypatch.setenv("PNRTE_SEG_BULK", bulk)
+    monkeypatch.setenv("PNRTE_SEG_PAD", "0")
     from paper_1807_00410_b200 import _lib
     from paper_1807_00410_b200.solver import PnContext
     spec = rand_spec(N, res, 31)
@@ -189,6 +197,37 @@ def test_loopback_slabs_match_single_slab(N, res, slabs, bulk, monkeypatch):
     _lib.check(L.pn_group_solve(hs, slabs, ctypes.byref(opts), xp, ctypes.byref(rep), None, None, 0, None))
     assert rep.iterations == ro.iterations
     assert torch.equal(torch.cat(xs), xo)
+
+
+@pytest.mark.parametrize("N,res", [(1, (7, 5, 6)), (3, (33, 6, 5)), (5, (40, 9, 7)), (7, (17, 4, 5)), (2, (65, 3, 4))])
+def test_padded_segmented_path(N, res, monkeypatch):
+    """nx % 32 != 0 on one slab: the segmented operator on the zero-padded
+    solve layout (last 32-voxel row partial) against the table operator
+    (PNRTE_SEG_PAD=0) and the C oracle, for A, A^T, the fused reductions
+    (solve) and Jacobi: products within rounding, solves to the same
+    iteration count and field."""
+    from oracle.oracle import StencilOracle
+    from paper_1807_00410_b200.solver import PnContext
+    spec = rand_spec(N, res, 55 + N)
+    t = build_tables(N)
+    out = {}
+    for pad in ("1", "0"):
+        monkeypatch.setenv("PNRTE_SEG_PAD", pad)
+        c = PnContext(t, res, spec.h)
+        c.set_fields(spec)
+        x = np.random.default_rng(9).normal(size=c.R_local)
+        ys = [c.apply(x, tr, "fast").cpu().numpy() for tr in (0, 1)]
+        sols = [c.solve(tol=1e-10, max_iter=3000, jacobi=j, mode="fast") for j in (False, True)]
+        out[pad] = (ys, sols)
+    o = StencilOracle(t, spec)
+    for tr in (0, 1):
+        want = o.apply(np.random.default_rng(9).normal(size=o.R), bool(tr))
+        assert rel(out["1"][0][tr], want) <= 1e-13
+        assert rel(out["1"][0][tr], out["0"][0][tr]) <= 1e-13
+    for (xa, ra), (xb, rb) in zip(out["1"][1], out["0"][1]):
+        assert ra.converged and rb.converged
+        assert abs(ra.iterations - rb.iterations) <= 1
+        assert rel(xa.cpu().numpy(), xb.cpu().numpy()) <= 1e-8
 
 
 # ---------------------------------------------------------------------------
