@@ -36,12 +36,19 @@ struct SegRow {
     const double *diag;                     // stored diagonal row + lane (DIAG_ARRAY)
     int lane;
     bool bx, bx_p, by, bz, by_p, bz_p;      // last-face flags: own voxel, x+1, y+1 row, z+1 row
-    bool xpad;                              // lane beyond nx in a zero-padded last row (output 0)
     static constexpr bool ysm = false;      // y-neighbour rows always in global memory
+    static constexpr bool padx = false;     // no zero-padded lanes
 };
 // bulk path: a y-neighbour row may be a staged row of this CTA (shared memory)
 struct SegRowY : SegRow {
     static constexpr bool ysm = true;
+};
+// nx % 32 != 0: the last row of each x-line is zero-padded; its padding lanes
+// (xpad) output 0 (separate instantiation, so unpadded grids pay nothing)
+template <class Base>
+struct SegRowPad : Base {
+    bool xpad;
+    static constexpr bool padx = true;
 };
 
 struct RedAcc {
@@ -308,7 +315,7 @@ __device__ __forceinline__ void seg_pair_sync(int rw) {
 }
 
 // compute one staged row: outputs (and fused reduction terms) of this warp's classes
-template <int N, int TRANS, int RED, bool JAC, bool TMA>
+template <int N, int TRANS, int RED, bool JAC, bool TMA, bool PAD>
 __device__ __forceinline__ void seg_compute(const SegParams &prm, const SegGeo &g, const SegItem &it,
                                             const double *xs, const double *__restrict__ X, double *__restrict__ Y,
                                             int rw,
@@ -317,7 +324,8 @@ __device__ __forceinline__ void seg_compute(const SegParams &prm, const SegGeo &
     constexpr int U = (N + 1) * (N + 1);
     constexpr long long rowlen = (long long)U * 32;
     const int i = it.seg * 32 + lane;
-    std::conditional_t<TMA, SegRowY, SegRow> r;
+    using RowB = std::conditional_t<TMA, SegRowY, SegRow>;
+    std::conditional_t<PAD, SegRowPad<RowB>, RowB> r;
     r.lane = lane;
     r.xs = xs + lane;
     r.eprev = xs + 32 * U;
@@ -337,7 +345,7 @@ __device__ __forceinline__ void seg_compute(const SegParams &prm, const SegGeo &
     r.minv = minv ? minv + it.rowbase + lane : nullptr;
     r.zt = zt ? zt + it.rowbase + lane : nullptr;
     r.diag = nullptr;
-    r.xpad = i >= g.nx;
+    if constexpr (PAD) r.xpad = i >= g.nx;
     r.bx = i == g.nx - 1;
     r.bx_p = i + 1 == g.nx - 1;
     r.by = it.j == g.ny - 1;
@@ -395,7 +403,7 @@ __device__ __forceinline__ void seg_partial(const SegGeo &g, const SegItem &it, 
 // rows, and the row of the CTA PN_SEG_PF places ahead prefetched into L2.
 // TMA = false (L2-resident slabs, where the bulk path measured slower):
 // cp.async staging, all y/z neighbours from L2.
-template <int N, int TRANS, int RED, bool JAC, bool TMA>
+template <int N, int TRANS, int RED, bool JAC, bool TMA, bool PAD>
 __global__ void PN_SEG_BOUNDS(N) k_seg(
     const __grid_constant__ SegParams prm, SegGeo g, const double *__restrict__ X, double *__restrict__ Y,
     const double *__restrict__ minv, double *__restrict__ zt, const double *__restrict__ st,
@@ -438,7 +446,7 @@ __global__ void PN_SEG_BOUNDS(N) k_seg(
             if (rw > 0) mbar_wait(seg_bar<N>(xs - SW), 0);
             if (rw < SegTune<N>::rows - 1 && it.j + 1 < g.ny) mbar_wait(seg_bar<N>(xs + SW), 0);
         }
-        seg_compute<N, TRANS, RED, JAC, TMA>(prm, g, it, xs, X, Y, rw, minv, zt, lane, half, ra);
+        seg_compute<N, TRANS, RED, JAC, TMA, PAD>(prm, g, it, xs, X, Y, rw, minv, zt, lane, half, ra);
     }
     seg_partial<N, RED, JAC>(g, it, ra, lane, warp, partials, slot_stride, rb);
 }
@@ -458,15 +466,20 @@ int seg_launch(const SegParams &prm, const SegGeo &g0, int trans, int red, bool 
     dim3 grid((unsigned)nblk), block(SegTune<N>::threads);
     const size_t smem = rows * seg_smem_per_warp<N>();
     if (g.nyb != (g.ny + rows - 1) / rows) { set_error("segmented launch: row blocking mismatch"); return PN_ERR_INVALID; }
-#define PN_SEG_GO2(T, R, J, B)                                                                                  \
-    do {                                                                                                        \
-        static bool cfg_done = false;                                                                           \
-        if (!cfg_done) {                                                                                        \
-            cudaFuncSetAttribute(k_seg<N, T, R, J, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-            cfg_done = true;                                                                                    \
-        }                                                                                                       \
-        k_seg<N, T, R, J, B><<<grid, block, smem, s>>>(prm, g, x, y, minv, zt, st, ss, partials, slot_stride, rb, \
-                                                       state);                                                  \
+#define PN_SEG_GO3(T, R, J, B, P)                                                                                 \
+    do {                                                                                                          \
+        static bool cfg_done = false;                                                                             \
+        if (!cfg_done) {                                                                                          \
+            cudaFuncSetAttribute(k_seg<N, T, R, J, B, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+            cfg_done = true;                                                                                      \
+        }                                                                                                         \
+        k_seg<N, T, R, J, B, P><<<grid, block, smem, s>>>(prm, g, x, y, minv, zt, st, ss, partials, slot_stride,  \
+                                                          rb, state);                                             \
+    } while (0)
+#define PN_SEG_GO2(T, R, J, B)                        \
+    do {                                              \
+        if (g.sx != g.nx) PN_SEG_GO3(T, R, J, B, true); \
+        else PN_SEG_GO3(T, R, J, B, false);           \
     } while (0)
 #define PN_SEG_GO(T, R, J)                     \
     do {                                       \
@@ -485,6 +498,7 @@ int seg_launch(const SegParams &prm, const SegGeo &g0, int trans, int red, bool 
         }
     }
 #undef PN_SEG_GO2
+#undef PN_SEG_GO3
 #undef PN_SEG_GO
     PN_CUDA(cudaGetLastError());
     return PN_OK;
