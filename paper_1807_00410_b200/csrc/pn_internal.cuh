@@ -141,6 +141,8 @@ struct pn_context {
     double *partials = nullptr;   // [RED_SLOTS][nz][red_bx] block partials (global plane index)
     double *plane_sums = nullptr; // [RED_SLOTS][nz] level-1 sums (all-gathered across ranks)
     unsigned *counter = nullptr;  // finished-block count of the fused plane-sum / scalar launch
+    double *small_parts = nullptr;// [4][SMALL_MAX_BLOCKS] block partials of the one-launch small solve
+    double *small_vecs = nullptr; // [2][R_l] second p and r buffers of the one-launch small solve
     double *ddot_chunks = nullptr;// faithful ddot chunk results [4][64]
     pn::State *state = nullptr;   // device
     pn::State *h_state = nullptr; // pinned host mirror
@@ -253,5 +255,11 @@ enum Scalar {
     S_FINAL,           // zz = slot 0, rr = slot 3 (true residuals)
 };
 int launch_scalar(pn_context *c, int which, int faithful, int blas_threads, cudaStream_t s);
+
+// Small single-slab fast solves: the whole CGNR iteration loop in one
+// cooperative launch (reference layout, table operator).
+constexpr int SMALL_MAX_BLOCKS = 2048;
+int launch_cg_small(pn_context *c, bool jacobi, cudaStream_t s);
+int cg_small_capacity(pn_context *c, long long *rows);
 
 }  // namespace pn

@@ -16,10 +16,15 @@
 #include <cstdint>
 #include <math.h>
 
+#include <algorithm>
+#include <cooperative_groups.h>
+
 #include "pn_internal.cuh"
 #include "pn_seg_types.cuh"
 
 namespace pn {
+
+namespace cg = cooperative_groups;
 
 __device__ __forceinline__ bool stopped(const State *st) { return *(volatile const int *)&st->done != 0; }
 
@@ -847,6 +852,283 @@ int launch_scalar(pn_context *c, int which, int faithful, int blas_threads, cuda
     a.hist_len = c->hist_len;
     k_scalar<<<1, 256, 0, s>>>(which, a, c->state);
     PN_CUDA(cudaGetLastError());
+    c->launches++;
+    return PN_OK;
+}
+
+// ------------------------------------------------- small-system CGNR --
+// Fast CGNR (solver.py:231-253) for systems whose working set is a few MB:
+// there the graph-replayed chain of six launches per iteration is latency
+// bound (config 1: ~30 us per iteration).  One cooperative launch runs the
+// whole iteration loop: reference layout, the table operator (both A and A^T
+// tables resident in shared memory for the whole solve), grid barriers
+// between the four phases w = A p | x, r update | z = A^T r | p update.  Every
+// block sums the block partials in the same fixed order, so all blocks take
+// the same scalar decisions; block 0 writes the histories and, at the end,
+// the solver state.
+struct SmallTab {
+    double *w;
+    int *ptr, *oth, *dir, *isd, *dg;
+};
+
+__device__ void small_load_tab(const Tables &T, int trans, int U, const SmallTab &s) {
+    const int *p_ = trans ? T.t_ptr : T.a_ptr;
+    const int *o_ = trans ? T.t_src : T.a_tgt;
+    const int *d_ = trans ? T.t_dir : T.a_dir;
+    const int *i_ = trans ? T.t_diag : T.a_diag;
+    const double *w_ = trans ? T.t_w : T.a_w;
+    const int ne = p_[U];
+    for (int e = threadIdx.x; e < ne; e += blockDim.x) {
+        s.w[e] = w_[e]; s.oth[e] = o_[e]; s.dir[e] = d_[e]; s.isd[e] = i_[e];
+    }
+    for (int e = threadIdx.x; e <= U; e += blockDim.x) s.ptr[e] = p_[e];
+    for (int cc = threadIdx.x; cc < U; cc += blockDim.x) {
+        int dg = -1;
+        for (int e = p_[cc]; e < p_[cc + 1]; ++e)
+            if (i_[e]) dg = e;
+        s.dg[cc] = dg;
+    }
+}
+
+// operand of a phase, formed on the fly: v[i] = fma(s, a[i], b[i])
+// (p_new = zt + beta p_old in the A phase, r_new = r_old - alpha w in the A^T phase)
+struct SmallIn {
+    const double *a, *b;
+    double s;
+    __device__ __forceinline__ double operator()(long long i) const { return fma(s, a[i], b[i]); }
+};
+
+// one row of the fast table operator (as k_apply_table<false, RECOMPUTE>)
+template <bool RECOMPUTE>
+__device__ __forceinline__ double small_row(const SmallTab &s, const int *spar, const double *slamp, const Fields &F,
+                                            const Geo &g, const double *diag, const SmallIn &x, unsigned row,
+                                            double xrow, const FastDiv &du, const FastDiv &dnx, const FastDiv &dny) {
+    const int U = g.U;
+    const unsigned vox = fdiv(row, du);
+    const int c = (int)(row - vox * (unsigned)U);
+    const unsigned q = fdiv(vox, dnx);
+    const int i = (int)(vox - q * (unsigned)g.nx);
+    const unsigned k = fdiv(q, dny);
+    const int j = (int)(q - k * (unsigned)g.ny), kg = (int)k;
+    const bool pinned_c = (spar[c] & boundary_bits(g, i, j, kg)) != 0;
+    double sum = 0.0;
+    if (s.dg[c] >= 0) {
+        double a;
+        if (RECOMPUTE) {
+            const int pc = spar[c];
+            double st_ = 0.0, ss_ = 0.0;
+            int n = 0;
+            for (int t = 0; t < 8; ++t) {
+                if (t & ~pc) continue;
+                st_ += fsample(F, g, 0, i, j, kg, t);
+                ss_ += fsample(F, g, 1, i, j, kg, t);
+                ++n;
+            }
+            const double inv = 1.0 / n;
+            a = st_ * inv - slamp[c] * (ss_ * inv);
+        } else {
+            a = diag[row];
+        }
+        sum = a * xrow;
+    }
+    if (pinned_c) return sum;
+    for (int e = s.ptr[c]; e < s.ptr[c + 1]; ++e) {
+        if (s.isd[e]) continue;
+        const int d = s.dir[e], o = s.oth[e];
+        const int ii = i + c_dx[d], jj = j + c_dy[d], kk = kg + c_dz[d];
+        if (ii < 0 || jj < 0 || kk < 0 || ii >= g.nx || jj >= g.ny || kk >= g.nz) continue;
+        const int nbb = (ii == g.nx - 1) | ((jj == g.ny - 1) << 1) | ((kk == g.nz - 1) << 2);
+        if (spar[o] & nbb) continue;
+        sum = fma(s.w[e], x(((long long)kk * g.pvox + (long long)jj * g.nx + ii) * U + o), sum);
+    }
+    return sum;
+}
+
+// block tree of up to 2 values -> parts[slot * cap + blockIdx.x]
+__device__ __forceinline__ void small_block_sum(double a, double b, int nv, double *parts, int s0, int s1, int cap,
+                                                double *red) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int o = 16; o > 0; o >>= 1) {
+        a = __dadd_rn(a, __shfl_down_sync(0xffffffffu, a, o));
+        if (nv > 1) b = __dadd_rn(b, __shfl_down_sync(0xffffffffu, b, o));
+    }
+    if (lane == 0) { red[wid] = a; red[32 + wid] = b; }
+    __syncthreads();
+    if (wid == 0) {
+        const int nw = blockDim.x >> 5;
+        a = lane < nw ? red[lane] : 0.0;
+        b = lane < nw ? red[32 + lane] : 0.0;
+        for (int o = 16; o > 0; o >>= 1) {
+            a = __dadd_rn(a, __shfl_down_sync(0xffffffffu, a, o));
+            if (nv > 1) b = __dadd_rn(b, __shfl_down_sync(0xffffffffu, b, o));
+        }
+        if (lane == 0) {
+            parts[s0 * cap + blockIdx.x] = a;
+            if (nv > 1) parts[s1 * cap + blockIdx.x] = b;
+        }
+    }
+    __syncthreads();
+}
+
+// fixed-order sum of the nb partials of a slot (identical in every block)
+__device__ __forceinline__ double small_grid_sum(const double *parts, int slot, int cap, double *red) {
+    double a = 0.0;
+    for (int t = threadIdx.x; t < (int)gridDim.x; t += blockDim.x) a = __dadd_rn(a, __ldcg(parts + slot * cap + t));
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int o = 16; o > 0; o >>= 1) a = __dadd_rn(a, __shfl_xor_sync(0xffffffffu, a, o));
+    if (lane == 0) red[64 + wid] = a;
+    __syncthreads();
+    double r = 0.0;
+    for (int w_ = 0; w_ < (int)(blockDim.x >> 5); ++w_) r = __dadd_rn(r, red[64 + w_]);
+    __syncthreads();
+    return r;
+}
+
+static size_t small_smem(const pn_context *c) {
+    const size_t na = c->tb.n_a, nt = c->tb.n_t, U = c->U;
+    return (na + nt + U + 96) * sizeof(double) + (2 * (U + 1) + 3 * (na + nt) + 3 * U) * sizeof(int);
+}
+
+template <bool RECOMPUTE>
+__global__ void __launch_bounds__(256, 4) k_cg_small(Tables T, Fields F, Geo g, const double *diag, double *x, double *r,
+                                                  double *p, double *w, double *z, double *zt, const double *minv,
+                                                  double *p2, double *r2, double *parts, int cap, State *st, double *hist_n, double *hist_p,
+                                                  long long hist_len, FastDiv du, FastDiv dnx, FastDiv dny) {
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int U = g.U, na = T.n_a, nt = T.n_t;
+    double *dp = (double *)smem_raw;
+    SmallTab ta, tt;
+    ta.w = dp; tt.w = dp + na;
+    double *slamp = dp + na + nt, *red = slamp + U;
+    int *ip = (int *)(red + 96);
+    ta.ptr = ip; ta.oth = ta.ptr + U + 1; ta.dir = ta.oth + na; ta.isd = ta.dir + na; ta.dg = ta.isd + na;
+    tt.ptr = ta.dg + U; tt.oth = tt.ptr + U + 1; tt.dir = tt.oth + nt; tt.isd = tt.dir + nt; tt.dg = tt.isd + nt;
+    int *spar = tt.dg + U;
+    small_load_tab(T, 0, U, ta);
+    small_load_tab(T, 1, U, tt);
+    for (int e = threadIdx.x; e < U; e += blockDim.x) { spar[e] = T.par[e]; slamp[e] = T.lamp[e]; }
+    __syncthreads();
+
+    const unsigned R = (unsigned)(g.plane * g.nzl);
+    const unsigned nth = gridDim.x * blockDim.x, tid = blockIdx.x * blockDim.x + threadIdx.x;
+    const double *ZT = zt ? zt : z;
+    double rho = st->rho, alpha = st->alpha, beta = 0.0, ww = st->ww, zz = st->zz, zzt = st->zzt, rr = st->rr;
+    const double tol = st->tol, primal_tol = st->primal_tol, norm_atb = st->norm_atb, norm_b = st->norm_b;
+    long long it = st->it;
+    const long long max_iter = st->max_iter;
+    int converged = 0, zero_ww = 0;
+    // p and r double-buffered: each phase forms its operand on the fly from the
+    // previous buffer and writes the updated vector of its own rows to the other,
+    // so an iteration is two phases and two grid barriers.  p starts as zt
+    // (fma(0, p, zt) = zt).
+    double *pa = p, *pb = p2, *ra = r, *rb = r2;
+    while (true) {
+        // p = zt + beta p ; w = A p ; ww
+        double a0 = 0.0;
+        const SmallIn inp{pa, ZT, beta};
+        for (unsigned row = tid; row < R; row += nth) {
+            const double pn = inp(row);
+            pb[row] = pn;
+            const double v = small_row<RECOMPUTE>(ta, spar, slamp, F, g, diag, inp, row, pn, du, dnx, dny);
+            w[row] = v;
+            a0 = fma(v, v, a0);
+        }
+        small_block_sum(a0, 0.0, 1, parts, 0, 0, cap, red);
+        grid.sync();
+        ww = small_grid_sum(parts, 0, cap, red);
+        if (ww == 0.0) { zero_ww = 1; break; }
+        alpha = rho / ww;
+        // x += alpha p ; r -= alpha w ; z = A^T r ; zt = z * minv ; zz, z.zt, rr
+        double a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        const SmallIn inr{w, ra, -alpha};
+        for (unsigned row = tid; row < R; row += nth) {
+            x[row] = fma(alpha, pb[row], x[row]);
+            const double rn = inr(row);
+            rb[row] = rn;
+            a3 = fma(rn, rn, a3);
+            const double v = small_row<RECOMPUTE>(tt, spar, slamp, F, g, diag, inr, row, rn, du, dnx, dny);
+            z[row] = v;
+            const double t = minv ? v * minv[row] : v;
+            if (zt) zt[row] = t;
+            a2 = fma(v, t, a2);
+            a1 = fma(v, v, a1);
+        }
+        small_block_sum(a1, a2, 2, parts, 1, 2, cap, red);
+        small_block_sum(a3, 0.0, 1, parts, 3, 3, cap, red);
+        grid.sync();
+        zz = small_grid_sum(parts, 1, cap, red);
+        zzt = small_grid_sum(parts, 2, cap, red);
+        rr = small_grid_sum(parts, 3, cap, red);
+        ++it;
+        const double normal_rel = sqrt(zz) / norm_atb, primal_rel = sqrt(rr) / norm_b;
+        if (blockIdx.x == 0 && threadIdx.x == 0 && it - 1 < hist_len) {
+            hist_n[it - 1] = normal_rel;
+            hist_p[it - 1] = primal_rel;
+        }
+        if (normal_rel <= tol && (primal_tol < 0.0 || primal_rel <= primal_tol)) { converged = 1; break; }
+        beta = rho != 0.0 ? zzt / rho : 0.0;
+        rho = zzt;
+        if (it >= max_iter) break;
+        double *t0 = pa; pa = pb; pb = t0;
+        double *t1 = ra; ra = rb; rb = t1;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        st->rho = rho; st->alpha = alpha; st->beta = beta;
+        st->ww = ww; st->zz = zz; st->zzt = zzt; st->rr = rr;
+        st->it = it;
+        st->converged = converged;
+        st->zero_ww = zero_ww;
+        st->done = 1;
+        st->xupd = 0;
+    }
+}
+
+// rows the one-launch solve covers with one row per resident thread (its
+// per-iteration time doubles beyond that; profiles/r01_coop_probe.jsonl)
+int cg_small_capacity(pn_context *c, long long *rows) {
+    const bool recompute = c->canonical_diag && c->uniform_phase;
+    auto kern = recompute ? k_cg_small<true> : k_cg_small<false>;
+    const size_t sm = small_smem(c);
+    if (sm > 48 * 1024) PN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    int per_sm = 0, nsm = 0;
+    PN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, sm));
+    PN_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
+    *rows = (long long)std::min(per_sm * nsm, SMALL_MAX_BLOCKS) * 256;
+    return PN_OK;
+}
+
+int launch_cg_small(pn_context *c, bool jacobi, cudaStream_t s) {
+    const Geo g = c->g;
+    const long long R = g.plane * g.nzl;
+    if (R >= (1LL << 31) || g.nzl != g.nz) { set_error("internal: small solve needs one slab < 2^31 rows"); return PN_ERR_INVALID; }
+    const bool recompute = c->canonical_diag && c->uniform_phase;
+    if (!recompute && !c->diag_ready) { set_error("internal: diagonal not assembled"); return PN_ERR_INVALID; }
+    auto kern = recompute ? k_cg_small<true> : k_cg_small<false>;
+    const size_t sm = small_smem(c);
+    if (sm > 48 * 1024) PN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    int per_sm = 0, nsm = 0;
+    PN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, sm));
+    PN_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
+    if (per_sm < 1) { set_error("small solve: kernel does not fit on an SM"); return PN_ERR_UNSUPPORTED; }
+    int nb = (int)std::min<long long>((long long)per_sm * nsm, (R + 255) / 256);
+    nb = std::max(1, std::min(nb, SMALL_MAX_BLOCKS));
+    Tables T = c->tb;
+    Fields F = c->f;
+    const double *diag = c->diag;
+    double *x = c->x.p, *r = c->r.p, *p = c->p.p, *w = c->w.p, *z = c->z.p;
+    double *zt = jacobi ? c->zt.p : nullptr;
+    const double *minv = jacobi ? c->minv.p : nullptr;
+    double *p2 = c->small_vecs, *r2 = c->small_vecs + R;
+    double *parts = c->small_parts;
+    int cap = SMALL_MAX_BLOCKS;
+    State *st = c->state;
+    double *hn = c->hist_n, *hp = c->hist_p;
+    long long hl = c->hist_len;
+    FastDiv du = make_fastdiv((unsigned)c->U), dnx = make_fastdiv((unsigned)g.nx), dny = make_fastdiv((unsigned)g.ny);
+    void *args[] = {&T, &F, (void *)&g, &diag, &x, &r, &p, &w, &z, &zt, &minv, &p2, &r2, &parts, &cap, &st, &hn, &hp, &hl,
+                    &du, &dnx, &dny};
+    PN_CUDA(cudaLaunchCooperativeKernel((const void *)kern, nb, 256, args, sm, s));
     c->launches++;
     return PN_OK;
 }

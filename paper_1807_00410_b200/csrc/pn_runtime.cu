@@ -783,6 +783,23 @@ static int from_solve_layout(pn_context *c, bool seg, const double *src, double 
     return PN_OK;
 }
 
+// Fast single-slab solves run their iteration loop as one cooperative launch
+// (launch_cg_small) when every row has its own resident thread (about 150 k
+// rows on a B200) and the operator has at most 2^20 table entries in all: past
+// that the graph-replayed segmented chain is faster (profiles/r01_coop_probe.jsonl:
+// P3 20^3 36.8 vs 28.6 us per iteration).  PNRTE_SMALL_MAX sets a row limit
+// instead, 0 disables.
+static bool use_small(const std::vector<pn_context *> &cs, const pn_solve_opts *o) {
+    if (o->mode == 1 || cs.size() != 1 || o->max_iter <= 0) return false;
+    pn_context *c = cs[0];
+    if (c->world > 1 || c->is_csr || c->g.nzl != c->g.nz || c->R_l() >= (1LL << 31)) return false;
+    if (const char *e = getenv("PNRTE_SMALL_MAX")) return c->R_l() <= atoll(e);
+    long long cap = 0;
+    if (cg_small_capacity(c, &cap) != PN_OK) return false;
+    const long long nvox = c->R_l() / c->U;
+    return c->R_l() <= cap && nvox * c->tb.n_a <= (1LL << 20);
+}
+
 static int solve_group(std::vector<pn_context *> &cs, const pn_solve_opts *o, const double *const *bs,
                        const double *const *x0s, double *const *xs, pn_report *rep, double *hn, double *hp,
                        int64_t cap, cudaStream_t s) {
@@ -794,7 +811,8 @@ static int solve_group(std::vector<pn_context *> &cs, const pn_solve_opts *o, co
     if (F && c0->world > 1) { set_error("faithful mode is single-slab only"); return PN_ERR_UNSUPPORTED; }
     if (F && (o->blas_threads < 1 || o->blas_threads > 64)) { set_error("blas_threads out of range"); return PN_ERR_INVALID; }
     const bool jacobi = o->jacobi != 0;
-    bool seg = !F;
+    const bool small = use_small(cs, o);
+    bool seg = !F && !small;
     for (auto *c : cs) seg = seg && pn_seg_ok(c);
     SegActive seg_active(cs, seg);
     for (auto *c : cs) {
@@ -864,7 +882,12 @@ static int solve_group(std::vector<pn_context *> &cs, const pn_solve_opts *o, co
     // (kernels past the stop are predicated no-ops).
     if (o->max_iter > 0) {
         const bool graph = cs.size() == 1 && c0->world <= 1 && o->check_every >= 0;
-        if (graph) {
+        if (small) {
+            if (!(c0->canonical_diag && c0->uniform_phase)) PN_TRY(ensure_diag(c0, s));
+            if (!c0->small_parts) PN_TRY(dalloc(c0, &c0->small_parts, (size_t)4 * SMALL_MAX_BLOCKS));
+            if (!c0->small_vecs) PN_TRY(dalloc(c0, &c0->small_vecs, (size_t)2 * c0->R_l()));
+            PN_TRY(launch_cg_small(c0, jacobi, s));
+        } else if (graph) {
             PN_TRY(run_graph_batches(c0, o, jacobi, seg, s));
         } else {
             long long batch = o->check_every > 0 ? o->check_every : 4;

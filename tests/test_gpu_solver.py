@@ -167,6 +167,7 @@ def test_loopback_slabs_match_single_slab(N, res, slabs, bulk, monkeypatch):
     import torch
     monkeypatch.setenv("PNRTE_SEG_BULK", bulk)
     monkeypatch.setenv("PNRTE_SEG_PAD", "0")
+    monkeypatch.setenv("PNRTE_SMALL_MAX", "0")   # the launch chain, as the slab group runs
     from paper_1807_00410_b200 import _lib
     from paper_1807_00410_b200.solver import PnContext
     spec = rand_spec(N, res, 31)
@@ -211,6 +212,7 @@ def test_padded_segmented_path(N, res, monkeypatch):
     spec = rand_spec(N, res, 55 + N)
     t = build_tables(N)
     out = {}
+    monkeypatch.setenv("PNRTE_SMALL_MAX", "0")   # the segmented solve, not the one-launch small path
     for pad in ("1", "0"):
         monkeypatch.setenv("PNRTE_SEG_PAD", pad)
         c = PnContext(t, res, spec.h)
