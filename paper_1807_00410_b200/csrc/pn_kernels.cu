@@ -970,18 +970,30 @@ __device__ __forceinline__ void small_block_sum(double a, double b, int nv, doub
     __syncthreads();
 }
 
-// fixed-order sum of the nb partials of a slot (identical in every block)
-__device__ __forceinline__ double small_grid_sum(const double *parts, int slot, int cap, double *red) {
-    double a = 0.0;
-    for (int t = threadIdx.x; t < (int)gridDim.x; t += blockDim.x) a = __dadd_rn(a, __ldcg(parts + slot * cap + t));
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    for (int o = 16; o > 0; o >>= 1) a = __dadd_rn(a, __shfl_xor_sync(0xffffffffu, a, o));
-    if (lane == 0) red[64 + wid] = a;
+// fixed-order sums of the nb partials of NS slots s0, s0+1, ... in one pass
+// (identical in every block)
+template <int NS>
+__device__ __forceinline__ void small_grid_sum(const double *parts, int s0, int cap, double *red, double *out) {
+    double a[NS];
+#pragma unroll
+    for (int q = 0; q < NS; ++q) a[q] = 0.0;
+    for (int t = threadIdx.x; t < (int)gridDim.x; t += blockDim.x)
+#pragma unroll
+        for (int q = 0; q < NS; ++q) a[q] = __dadd_rn(a[q], __ldcg(parts + (s0 + q) * cap + t));
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+    for (int q = 0; q < NS; ++q) {
+        for (int o = 16; o > 0; o >>= 1) a[q] = __dadd_rn(a[q], __shfl_xor_sync(0xffffffffu, a[q], o));
+        if (lane == 0) red[64 + q * 8 + wid] = a[q];
+    }
     __syncthreads();
-    double r = 0.0;
-    for (int w_ = 0; w_ < (int)(blockDim.x >> 5); ++w_) r = __dadd_rn(r, red[64 + w_]);
+#pragma unroll
+    for (int q = 0; q < NS; ++q) {
+        double r = 0.0;
+        for (int w_ = 0; w_ < nw; ++w_) r = __dadd_rn(r, red[64 + q * 8 + w_]);
+        out[q] = r;
+    }
     __syncthreads();
-    return r;
 }
 
 static size_t small_smem(const pn_context *c) {
@@ -1036,7 +1048,7 @@ __global__ void __launch_bounds__(256, 4) k_cg_small(Tables T, Fields F, Geo g, 
         }
         small_block_sum(a0, 0.0, 1, parts, 0, 0, cap, red);
         grid.sync();
-        ww = small_grid_sum(parts, 0, cap, red);
+        small_grid_sum<1>(parts, 0, cap, red, &ww);
         if (ww == 0.0) { zero_ww = 1; break; }
         alpha = rho / ww;
         // x += alpha p ; r -= alpha w ; z = A^T r ; zt = z * minv ; zz, z.zt, rr
@@ -1057,9 +1069,11 @@ __global__ void __launch_bounds__(256, 4) k_cg_small(Tables T, Fields F, Geo g, 
         small_block_sum(a1, a2, 2, parts, 1, 2, cap, red);
         small_block_sum(a3, 0.0, 1, parts, 3, 3, cap, red);
         grid.sync();
-        zz = small_grid_sum(parts, 1, cap, red);
-        zzt = small_grid_sum(parts, 2, cap, red);
-        rr = small_grid_sum(parts, 3, cap, red);
+        double sums[3];
+        small_grid_sum<3>(parts, 1, cap, red, sums);
+        zz = sums[0];
+        zzt = sums[1];
+        rr = sums[2];
         ++it;
         const double normal_rel = sqrt(zz) / norm_atb, primal_rel = sqrt(rr) / norm_b;
         if (blockIdx.x == 0 && threadIdx.x == 0 && it - 1 < hist_len) {

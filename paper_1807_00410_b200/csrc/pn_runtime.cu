@@ -785,8 +785,9 @@ static int from_solve_layout(pn_context *c, bool seg, const double *src, double 
 
 // Fast single-slab solves run their iteration loop as one cooperative launch
 // (launch_cg_small) when every row has its own resident thread (about 150 k
-// rows on a B200) and the operator has at most 2^20 table entries in all: past
-// that the graph-replayed segmented chain is faster (profiles/r01_coop_probe.jsonl:
+// rows on a B200) and, where the chain would run the segmented operator, the
+// operator has at most 2^20 table entries in all: past that the segmented
+// chain is faster (profiles/r01_coop_probe.jsonl:
 // P3 20^3 36.8 vs 28.6 us per iteration).  PNRTE_SMALL_MAX sets a row limit
 // instead, 0 disables.
 static bool use_small(const std::vector<pn_context *> &cs, const pn_solve_opts *o) {
@@ -797,7 +798,7 @@ static bool use_small(const std::vector<pn_context *> &cs, const pn_solve_opts *
     long long cap = 0;
     if (cg_small_capacity(c, &cap) != PN_OK) return false;
     const long long nvox = c->R_l() / c->U;
-    return c->R_l() <= cap && nvox * c->tb.n_a <= (1LL << 20);
+    return c->R_l() <= cap && (!pn_seg_ok(c) || nvox * c->tb.n_a <= (1LL << 20));
 }
 
 static int solve_group(std::vector<pn_context *> &cs, const pn_solve_opts *o, const double *const *bs,
