@@ -17,6 +17,7 @@
 #include <math.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cooperative_groups.h>
 
 #include "pn_internal.cuh"
@@ -1126,6 +1127,7 @@ int launch_cg_small(pn_context *c, bool jacobi, cudaStream_t s) {
     PN_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
     if (per_sm < 1) { set_error("small solve: kernel does not fit on an SM"); return PN_ERR_UNSUPPORTED; }
     int nb = (int)std::min<long long>((long long)per_sm * nsm, (R + 255) / 256);
+    if (const char *e = getenv("PNRTE_SMALL_GRID")) nb = atoi(e);   // test hook: force a grid size
     nb = std::max(1, std::min(nb, SMALL_MAX_BLOCKS));
     Tables T = c->tb;
     Fields F = c->f;
@@ -1142,7 +1144,14 @@ int launch_cg_small(pn_context *c, bool jacobi, cudaStream_t s) {
     FastDiv du = make_fastdiv((unsigned)c->U), dnx = make_fastdiv((unsigned)g.nx), dny = make_fastdiv((unsigned)g.ny);
     void *args[] = {&T, &F, (void *)&g, &diag, &x, &r, &p, &w, &z, &zt, &minv, &p2, &r2, &parts, &cap, &st, &hn, &hp, &hl,
                     &du, &dnx, &dny};
-    PN_CUDA(cudaLaunchCooperativeKernel((const void *)kern, nb, 256, args, sm, s));
+    const cudaError_t e = cudaLaunchCooperativeKernel((const void *)kern, nb, 256, args, sm, s);
+    if (e == cudaErrorCooperativeLaunchTooLarge) {
+        // SMs taken by other work (MPS, green contexts): the caller runs the launch chain
+        cudaGetLastError();
+        set_error("cooperative launch too large");
+        return PN_ERR_UNSUPPORTED;
+    }
+    PN_CUDA(e);
     c->launches++;
     return PN_OK;
 }

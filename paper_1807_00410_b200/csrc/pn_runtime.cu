@@ -887,7 +887,9 @@ static int solve_group(std::vector<pn_context *> &cs, const pn_solve_opts *o, co
             if (!(c0->canonical_diag && c0->uniform_phase)) PN_TRY(ensure_diag(c0, s));
             if (!c0->small_parts) PN_TRY(dalloc(c0, &c0->small_parts, (size_t)4 * SMALL_MAX_BLOCKS));
             if (!c0->small_vecs) PN_TRY(dalloc(c0, &c0->small_vecs, (size_t)2 * c0->R_l()));
-            PN_TRY(launch_cg_small(c0, jacobi, s));
+            const int st = launch_cg_small(c0, jacobi, s);
+            if (st == PN_ERR_UNSUPPORTED) PN_TRY(run_graph_batches(c0, o, jacobi, false, s));
+            else if (st != PN_OK) return st;
         } else if (graph) {
             PN_TRY(run_graph_batches(c0, o, jacobi, seg, s));
         } else {

@@ -109,3 +109,19 @@ def test_small_solve_repeatable(monkeypatch):
     a, ra, _ = _solve(spec, N, ALWAYS, monkeypatch, tol=1e-9, max_iter=3000)
     b, rb, _ = _solve(spec, N, ALWAYS, monkeypatch, tol=1e-9, max_iter=3000)
     assert ra.iterations == rb.iterations and a.tobytes() == b.tobytes()
+
+
+def test_small_solve_falls_back_when_grid_not_resident(monkeypatch):
+    """A cooperative grid larger than what is resident (other work on the SMs)
+    is refused by the driver; the solve then runs the launch chain on the same
+    reference-layout vectors instead of failing."""
+    from oracle.oracle import StencilOracle
+    N, res = 3, (16, 8, 8)
+    spec = rand_spec(N, res, 13)
+    monkeypatch.setenv("PNRTE_SMALL_GRID", "2048")   # > 4 CTAs x 148 SMs
+    xf, rf, lf = _solve(spec, N, ALWAYS, monkeypatch, tol=1e-10, max_iter=3000)
+    monkeypatch.delenv("PNRTE_SMALL_GRID")
+    xs, rs, ls = _solve(spec, N, ALWAYS, monkeypatch, tol=1e-10, max_iter=3000)
+    xo, ro = StencilOracle(build_tables(N), spec).cgnr(tol=1e-10, max_iter=3000)
+    assert rf.converged and abs(rf.iterations - ro["iterations"]) <= 1 and rel(xf, xo) <= 1e-8
+    assert lf > ls   # the chain ran
