@@ -656,6 +656,25 @@ int launch_ddot_emul(pn_context *c, const double *a, const double *b, long long 
     return PN_OK;
 }
 
+// Tree sum of sh[0..255] (blockDim.x == 256, sh written and synchronised) in
+// the order of `for o = 128..1: sh[t] += sh[t + o]`; the steps o <= 16 run in
+// warp 0's registers (shfl_down gives lane t the same two operands), so the
+// result is bit-identical with 3 block barriers instead of 8.  Valid in
+// thread 0; sh may be rewritten after the next __syncthreads.
+__device__ __forceinline__ double tree256(double *sh) {
+    for (int o = 128; o >= 32; o >>= 1) {
+        if (threadIdx.x < o) sh[threadIdx.x] = __dadd_rn(sh[threadIdx.x], sh[threadIdx.x + o]);
+        __syncthreads();
+    }
+    double a = 0.0;
+    if (threadIdx.x < 32) {
+        a = sh[threadIdx.x];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) a = __dadd_rn(a, __shfl_down_sync(0xffffffffu, a, o));
+    }
+    return a;
+}
+
 // ---------------------------------------------------------- plane sums --
 // Level 1 of every fast reduction: the block partials of one z-plane are
 // summed in a fixed order into plane_sums[slot][kg].  The scalar kernels sum
@@ -672,11 +691,8 @@ __global__ void __launch_bounds__(256) k_plane_sums(const double *__restrict__ p
     for (int i = threadIdx.x; i < cnt; i += blockDim.x) acc = __dadd_rn(acc, p[i]);
     sh[threadIdx.x] = acc;
     __syncthreads();
-    for (int o = 128; o > 0; o >>= 1) {
-        if (threadIdx.x < o) sh[threadIdx.x] = __dadd_rn(sh[threadIdx.x], sh[threadIdx.x + o]);
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) plane_sums[slot * nz + kg] = sh[0];
+    const double t = tree256(sh);
+    if (threadIdx.x == 0) plane_sums[slot * nz + kg] = t;
 }
 
 int launch_plane_sums(pn_context *c, int mask, int cnt, cudaStream_t s) {
@@ -708,11 +724,7 @@ __device__ double sum_slot(const ScalarArgs &a, int slot, double *sh) {
     for (long long i = threadIdx.x; i < a.n_part; i += blockDim.x) acc = __dadd_rn(acc, __ldcg(p + i));
     sh[threadIdx.x] = acc;
     __syncthreads();
-    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
-        if (threadIdx.x < o) sh[threadIdx.x] = __dadd_rn(sh[threadIdx.x], sh[threadIdx.x + o]);
-        __syncthreads();
-    }
-    double r = sh[0];
+    const double r = tree256(sh);   // blockDim.x == 256 (k_scalar, k_plane_sums_scalar); thread 0 uses it
     __syncthreads();
     return r;
 }
@@ -801,11 +813,9 @@ __global__ void __launch_bounds__(256) k_plane_sums_scalar(const double *__restr
         for (int i = threadIdx.x; i < n; i += blockDim.x) acc = __dadd_rn(acc, p[i]);
         sh[threadIdx.x] = acc;
         __syncthreads();
-        for (int o = 128; o > 0; o >>= 1) {
-            if (threadIdx.x < o) sh[threadIdx.x] = __dadd_rn(sh[threadIdx.x], sh[threadIdx.x + o]);
-            __syncthreads();
-        }
-        if (threadIdx.x == 0) plane_sums[slot * nz + kg] = sh[0];
+        const double t = tree256(sh);
+        if (threadIdx.x == 0) plane_sums[slot * nz + kg] = t;
+        __syncthreads();   // sh is reused by the scalar step
     }
     if (threadIdx.x == 0) {
         __threadfence();
