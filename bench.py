@@ -191,11 +191,18 @@ def paper_workloads(device):
         c.set_fields(spec)
         c.solve(tol=tol, max_iter=5)
         torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        _, rep = c.solve(tol=tol, max_iter=200000)
-        torch.cuda.synchronize()
-        sec = time.perf_counter() - t0
-        out[name] = {"seconds": sec, "iterations": rep.iterations, "converged": rep.converged, "tol": tol,
+        # median of 3 timed solves for the millisecond-scale problems (one sample
+        # of a 3 ms solve swings by 2x with host scheduling)
+        secs = []
+        while len(secs) < 3:
+            t0 = time.perf_counter()
+            _, rep = c.solve(tol=tol, max_iter=200000)
+            torch.cuda.synchronize()
+            secs.append(time.perf_counter() - t0)
+            if secs[0] > 1.0:
+                break
+        sec = float(np.median(secs))
+        out[name] = {"seconds": sec, "timed_solves": len(secs), "iterations": rep.iterations, "converged": rep.converged, "tol": tol,
                      "unknowns": c.R_local, "paper_cpu_seconds": paper_s, "paper_over_ours": paper_s / sec}
         del c
     return out

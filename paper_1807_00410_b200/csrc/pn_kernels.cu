@@ -1112,8 +1112,7 @@ __global__ void __launch_bounds__(256, 4) k_cg_small(Tables T, Fields F, Geo g, 
 // rows the one-launch solve covers with one row per resident thread (its
 // per-iteration time doubles beyond that; profiles/r01_coop_probe.jsonl)
 int cg_small_capacity(pn_context *c, long long *rows) {
-    const bool recompute = c->canonical_diag && c->uniform_phase;
-    auto kern = recompute ? k_cg_small<true> : k_cg_small<false>;
+    auto kern = k_cg_small<false>;   // the solve assembles the stored diagonal first
     const size_t sm = small_smem(c);
     if (sm > 48 * 1024) PN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     int per_sm = 0, nsm = 0;
@@ -1127,9 +1126,10 @@ int launch_cg_small(pn_context *c, bool jacobi, cudaStream_t s) {
     const Geo g = c->g;
     const long long R = g.plane * g.nzl;
     if (R >= (1LL << 31) || g.nzl != g.nz) { set_error("internal: small solve needs one slab < 2^31 rows"); return PN_ERR_INVALID; }
-    const bool recompute = c->canonical_diag && c->uniform_phase;
-    if (!recompute && !c->diag_ready) { set_error("internal: diagonal not assembled"); return PN_ERR_INVALID; }
-    auto kern = recompute ? k_cg_small<true> : k_cg_small<false>;
+    // the stored diagonal (assembled once, k_setup): one load per row instead of
+    // up to 16 site samples of sigma_t / sigma_s (12-18 % per iteration)
+    if (!c->diag_ready) { set_error("internal: diagonal not assembled"); return PN_ERR_INVALID; }
+    auto kern = k_cg_small<false>;
     const size_t sm = small_smem(c);
     if (sm > 48 * 1024) PN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     int per_sm = 0, nsm = 0;

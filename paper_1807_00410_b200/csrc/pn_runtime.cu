@@ -784,12 +784,12 @@ static int from_solve_layout(pn_context *c, bool seg, const double *src, double 
 }
 
 // Fast single-slab solves run their iteration loop as one cooperative launch
-// (launch_cg_small) when every row has its own resident thread (about 150 k
-// rows on a B200) and, where the chain would run the segmented operator, the
-// operator has at most 2^20 table entries in all: past that the segmented
-// chain is faster (profiles/r01_coop_probe.jsonl:
-// P3 20^3 36.8 vs 28.6 us per iteration).  PNRTE_SMALL_MAX sets a row limit
-// instead, 0 disables.
+// (launch_cg_small) when it beats the graph-replayed chain
+// (profiles/r01_coop_probe.jsonl): where the chain would run the table operator
+// too, up to one row per resident thread (about 150 k rows on a B200); against
+// the segmented chain, up to two rows per thread and 2^20 operator entries in
+// all (2^21 for N >= 4, whose chain costs ~45 us per iteration even at 8^3).
+// PNRTE_SMALL_MAX sets a row limit instead, 0 disables.
 static bool use_small(const std::vector<pn_context *> &cs, const pn_solve_opts *o) {
     if (o->mode == 1 || cs.size() != 1 || o->max_iter <= 0) return false;
     pn_context *c = cs[0];
@@ -797,8 +797,9 @@ static bool use_small(const std::vector<pn_context *> &cs, const pn_solve_opts *
     if (const char *e = getenv("PNRTE_SMALL_MAX")) return c->R_l() <= atoll(e);
     long long cap = 0;
     if (cg_small_capacity(c, &cap) != PN_OK) return false;
-    const long long nvox = c->R_l() / c->U;
-    return c->R_l() <= cap && (!pn_seg_ok(c) || nvox * c->tb.n_a <= (1LL << 20));
+    if (!pn_seg_ok(c)) return c->R_l() <= cap;
+    const long long entries = c->R_l() / c->U * c->tb.n_a;
+    return c->R_l() <= 2 * cap && entries <= (c->U > 16 ? (1LL << 21) : (1LL << 20));
 }
 
 static int solve_group(std::vector<pn_context *> &cs, const pn_solve_opts *o, const double *const *bs,
@@ -884,7 +885,7 @@ static int solve_group(std::vector<pn_context *> &cs, const pn_solve_opts *o, co
     if (o->max_iter > 0) {
         const bool graph = cs.size() == 1 && c0->world <= 1 && o->check_every >= 0;
         if (small) {
-            if (!(c0->canonical_diag && c0->uniform_phase)) PN_TRY(ensure_diag(c0, s));
+            PN_TRY(ensure_diag(c0, s));   // one load per row instead of up to 16 site samples
             if (!c0->small_parts) PN_TRY(dalloc(c0, &c0->small_parts, (size_t)4 * SMALL_MAX_BLOCKS));
             if (!c0->small_vecs) PN_TRY(dalloc(c0, &c0->small_vecs, (size_t)2 * c0->R_l()));
             const int st = launch_cg_small(c0, jacobi, s);
