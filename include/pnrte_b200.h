@@ -129,6 +129,14 @@ int pn_csr_export(pn_context *csr, int64_t *nnz, int64_t *indptr, int32_t *indic
 int pn_set_field(pn_context *ctx, int32_t slot, int32_t kind, double scalar,
                  const double *data, void *stream);
 
+/* Same for a z-range of the field: `data` holds the [i,j,k] C-order planes
+ * [k0, k0 + n_planes) of the global field (shape nx x ny x n_planes), which
+ * must cover the context's slab [z0, z0 + nz_local) and its +1 plane
+ * (clamped at nz).  One rank of a slab decomposition then never holds the
+ * global field (config 5: 1.07 GB per field at 512^3). */
+int pn_set_field_planes(pn_context *ctx, int32_t slot, int32_t kind, double scalar,
+                        const double *data, int32_t k0, int32_t n_planes, void *stream);
+
 /* Evaluate diagonal (when needed) and RHS Q from the fields (assemble()). */
 int pn_setup(pn_context *ctx, void *stream);
 

@@ -78,15 +78,16 @@ def _ptr(a):
 def blas_pin():
     """(threads, kernel) of this process's OpenBLAS, as the reference's numpy
     sees it (kernel 0 = SkylakeX, 1 = Haswell)."""
-    try:
-        from threadpoolctl import threadpool_info
-        for info in threadpool_info():
-            if info.get("internal_api") == "openblas":
-                arch = (info.get("architecture") or "").lower()
-                return int(info["num_threads"]), (1 if arch in ("haswell", "zen") else 0)
-    except Exception:
-        pass
-    return 1, 0
+    from threadpoolctl import threadpool_info
+    for info in threadpool_info():
+        if info.get("internal_api") == "openblas":
+            arch = (info.get("architecture") or "").lower()
+            if arch in ("haswell", "zen"):
+                return int(info["num_threads"]), 1
+            if arch == "skylakex":
+                return int(info["num_threads"]), 0
+            raise RuntimeError(f"oracle: no ddot emulation for OpenBLAS kernel {arch!r}")
+    raise RuntimeError("oracle: no OpenBLAS found; pass blas_threads / blas_kernel")
 
 
 def ddot(x, y, threads=8, kernel=0):
@@ -238,9 +239,11 @@ class CsrOracle:
 
     def cgnr(self, b, tol=1e-8, max_iter=50000, primal_tol=None, jacobi=False, x0=None,
              blas_threads=None, blas_kernel=None):
-        th, kn = blas_pin()
-        th = th if blas_threads is None else blas_threads
-        kn = kn if blas_kernel is None else blas_kernel
+        th, kn = (blas_threads, blas_kernel)
+        if th is None or kn is None:
+            pth, pkn = blas_pin()
+            th = pth if th is None else th
+            kn = pkn if kn is None else kn
 
         def jd():
             return np.asarray(self.A.multiply(self.A).sum(axis=0)).ravel()

@@ -90,6 +90,7 @@ def load():
         "pn_trilinear": [P, I32, P, I32, P, F64, I64, P, P, P],
         "pn_reconstruct": [P, I32, P, I32, P, P, F64, I64, P, I64, P, P, P],
         "pn_set_field": [P, I32, I32, F64, P, P],
+        "pn_set_field_planes": [P, I32, I32, F64, P, I32, I32, P],
         "pn_setup": [P, P],
         "pn_export_diag_rhs": [P, P, P, P],
         "pn_apply": [P, I32, I32, P, P, P],

@@ -18,6 +18,13 @@ quadrature projection (sh.py:220-223) as np.float64 scalars.
   cfg 5  P5 512^3 cfg-3 generator at 512^3, fixed 200 iterations
 Configs 3-5 contain vacuum (sigma_t = 0); converging solves use
 floor_sigma_t(spec, 1.0) (problems.py:87-97), throughput runs need no floor.
+
+Configs 3-5 take ``planes=(k0, k1)``: only the global z-planes [k0, k1) of
+every field are generated (the spec's ``z_planes``), bit-identical to the
+same planes of the whole grid -- the random draws are the small noise
+lattices and emitter positions, consumed in the same order either way.  A
+rank of a slab decomposition generates just its share (config 5: 1.07 GB
+per 512^3 field).
 """
 
 from __future__ import annotations
@@ -44,34 +51,44 @@ class Config:
     description: str
 
 
-def _spec(n, fields, name):
+def _spec(n, fields, name, planes=None):
+    zp = None if planes is None else (int(planes[0]), int(planes[1]) - int(planes[0]))
     return ProblemSpec(dim=3, origin=(-1.0,) * 3, extent=(2.0,) * 3, res=(n, n, n),
-                       fields=fields, bc="dirichlet", name=name)
+                       fields=fields, bc="dirichlet", name=name, z_planes=zp)
 
 
-def value_noise(rng, n, cells):
+def _zrange(n, planes):
+    k0, k1 = (0, n) if planes is None else (int(planes[0]), int(planes[1]))
+    if not (0 <= k0 < k1 <= n):
+        raise ValueError(f"planes {planes} outside 0..{n}")
+    return k0, k1
+
+
+def value_noise(rng, n, cells, planes=None):
     """Trilinear interpolation of a seeded (cells+1)^3 lattice, the pattern of
-    problems.py:178-192."""
+    problems.py:178-192 (z-planes [k0, k1) only when ``planes`` is given)."""
+    k0, k1 = _zrange(n, planes)
     lattice = rng.random((cells + 1,) * 3)
     t = np.linspace(0.0, cells, n, endpoint=False)
     i0 = np.floor(t).astype(int)
     frac = t - i0
     i1 = np.minimum(i0 + 1, cells)
-    out = np.zeros((n, n, n))
-    fx, fy, fz = frac[:, None, None], frac[None, :, None], frac[None, None, :]
+    out = np.zeros((n, n, k1 - k0))
+    fx, fy, fz = frac[:, None, None], frac[None, :, None], frac[None, None, k0:k1]
     for dx, wx in ((i0, 1 - fx), (i1, fx)):
         for dy, wy in ((i0, 1 - fy), (i1, fy)):
-            for dz, wz in ((i0, 1 - fz), (i1, fz)):
+            for dz, wz in ((i0[k0:k1], 1 - fz), (i1[k0:k1], fz)):
                 out += (wx * wy * wz) * lattice[np.ix_(dx, dy, dz)]
     return out
 
 
-def cloud_density(rng, n, base_period, octaves=4, persistence=0.5, cut=0.4):
+def cloud_density(rng, n, base_period, octaves=4, persistence=0.5, cut=0.4, planes=None):
+    k0, k1 = _zrange(n, planes)
     amps = [persistence ** o for o in range(octaves)]
-    noise = np.zeros((n, n, n))
+    noise = np.zeros((n, n, k1 - k0))
     for o in range(octaves):
         cells = max(1, (n * (2 ** o)) // base_period)
-        noise += amps[o] * value_noise(rng, n, cells)
+        noise += amps[o] * value_noise(rng, n, cells, planes)
     noise /= sum(amps)
     return np.clip((noise - cut) / (1.0 - cut), 0.0, 1.0)
 
@@ -105,39 +122,44 @@ def config2(seed=0, n=64):
                   f"P3 {n}^3 heterogeneous box-filtered sigma_t in [1,20] albedo U[0.5,0.99) g=0.3")
 
 
-def config3(seed=0, n=128, base_period=None):
+def config3(seed=0, n=128, base_period=None, planes=None):
     N = 5
+    k0, k1 = _zrange(n, planes)
     rng = np.random.default_rng(seed)
     bp = base_period if base_period is not None else max(1, n // 4)
-    st = 50.0 * cloud_density(rng, n, bp)
+    st = 50.0 * cloud_density(rng, n, bp, planes=planes)
     fields = {"sigma_t": st, "sigma_s": 0.95 * st}
     pe = phase_fields(0.9, N)
     for l in range(N + 1):
-        q = np.zeros((n, n, n))
-        q[:, :, 0] = float(pe[f"p_{l}"])
+        q = np.zeros((n, n, k1 - k0))
+        if k0 == 0:
+            q[:, :, 0] = float(pe[f"p_{l}"])
         fields[q_name(l, 0)] = q
     fields.update(phase_fields(0.6, N))
-    return Config(3, N, _spec(n, fields, "cfg3"), 1e-6, 50000, 1.0,
+    return Config(3, N, _spec(n, fields, "cfg3", planes), 1e-6, 50000, 1.0,
                   f"P5 {n}^3 4-octave cloud (period {bp}) sigma_t in [0,50] albedo 0.95 g=0.6 z=0 slab")
 
 
-def config4(seed=0, n=256):
+def config4(seed=0, n=256, planes=None):
     N = 7
+    k0, k1 = _zrange(n, planes)
     rng = np.random.default_rng(seed)
-    st = 100.0 * cloud_density(rng, n, max(1, n // 4))
+    st = 100.0 * cloud_density(rng, n, max(1, n // 4), planes=planes)
     h = 2.0 / n
-    q = np.zeros((n, n, n))
+    q = np.zeros((n, n, k1 - k0))
     lo, hi = (8, n - 8) if n > 24 else (0, n - 1)
     for (i, j, k) in rng.integers(lo, hi, (4, 3)):
-        q[i:i + 2, j:j + 2, k:k + 2] += 1.0 / (8 * h ** 3 * SQRT_4PI)
+        for kk in range(k, k + 2):        # emitters overlapping [k0, k1)
+            if k0 <= kk < k1:
+                q[i:i + 2, j:j + 2, kk - k0] += 1.0 / (8 * h ** 3 * SQRT_4PI)
     fields = {"sigma_t": st, "sigma_s": 0.99 * st, q_name(0, 0): q}
     fields.update(phase_fields(0.8, N))
-    return Config(4, N, _spec(n, fields, "cfg4"), 1e-6, 50000, 1.0,
+    return Config(4, N, _spec(n, fields, "cfg4", planes), 1e-6, 50000, 1.0,
                   f"P7 {n}^3 4-octave cloud sigma_t in [0,100] albedo 0.99 g=0.8 four 2^3 emitters")
 
 
-def config5(seed=0, n=512):
-    c = config3(seed=seed, n=n, base_period=n // 4)
+def config5(seed=0, n=512, planes=None):
+    c = config3(seed=seed, n=n, base_period=n // 4, planes=planes)
     return Config(5, 5, c.spec, 1e-300, 200, None,
                   f"P5 {n}^3 cfg-3 generator, fixed 200 iterations")
 

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/pnrte_b200.h"
@@ -165,11 +166,14 @@ struct pn_context {
     cudaGraphExec_t gexec = nullptr;
     long long gkey = -1;           // (mode, jacobi, seg, batch) the graph was captured for
     long long graph_launches = 0;  // kernels per graph replay
+    long long gen = 0;             // bumped whenever captured arguments may change (drop_graph)
+    std::vector<std::pair<pn_context *, long long>> gmembers;   // (context, gen) the graph captured
 
     // segmented fast path (pn_seg.cu)
     void *seg = nullptr;
     pn::Buf bs;                   // RHS in the solve layout
     std::vector<double> h_aw, h_tw;
+    std::vector<int> h_aptr, h_atgt, h_adir, h_adiag, h_tptr, h_tsrc, h_tdir, h_tdiag;   // structure checks
     // residual (RHS) term program on the host: comps whose terms use only
     // constant factors get their value once per setup (k_setup skips them)
     std::vector<int> h_rptr, h_hascoef, h_nf, h_tf;
@@ -198,7 +202,12 @@ namespace pn {
 
 // kernels (pn_kernels.cu)
 int launch_fill(double *p, long long n, double v, cudaStream_t s);
-int launch_field_slab(pn_context *c, int slot, const double *src, double *dst, cudaStream_t s);
+// p[i] = uniform [-1, 1) from a hash of (seed, offset + i): dense deterministic
+// bench inputs, identical for any slab decomposition (offset = global index)
+int launch_fill_hash(double *p, long long n, long long offset, unsigned long long seed, cudaStream_t s);
+// src: [i,j,k] C-order planes [src_k0, src_k0 + src_nk) of the field (src_nk <= 0: all nz planes)
+int launch_field_slab(pn_context *c, int slot, const double *src, double *dst, cudaStream_t s, int src_k0 = 0,
+                      int src_nk = 0);
 int launch_setup(pn_context *c, bool want_diag, bool want_rhs, cudaStream_t s, double *rhs_out = nullptr, int pin = 1);
 int launch_apply_table(pn_context *c, int trans, int faithful, int squared, const double *x, double *y, int red,
                        const double *minv, double *zt, cudaStream_t s, bool gated, int kl0 = 0, int npl = -1,

@@ -34,7 +34,7 @@ __device__ __forceinline__ bool stopped(const State *st) { return *(volatile con
 // k = min(z0+kl, nz-1), the +1 plane is the edge-replicated sample of
 // solver.py:62-64), x fastest.  32x32 smem transpose per j.
 __global__ void k_field_slab(const double *__restrict__ src, double *__restrict__ dst, int nx, int ny, int nz,
-                             int z0, int nplanes) {
+                             int z0, int nplanes, int src_k0, int src_nk) {
     __shared__ double tile[32][33];
     const int j = blockIdx.z;
     const int i0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
@@ -42,7 +42,7 @@ __global__ void k_field_slab(const double *__restrict__ src, double *__restrict_
         int i = i0 + r, kl = k0 + threadIdx.x;
         if (i < nx && kl < nplanes) {
             int kg = min(z0 + kl, nz - 1);
-            tile[r][threadIdx.x] = src[((long long)i * ny + j) * nz + kg];
+            tile[r][threadIdx.x] = src[((long long)i * ny + j) * src_nk + (kg - src_k0)];
         }
     }
     __syncthreads();
@@ -52,11 +52,13 @@ __global__ void k_field_slab(const double *__restrict__ src, double *__restrict_
     }
 }
 
-int launch_field_slab(pn_context *c, int slot, const double *src, double *dst, cudaStream_t s) {
+int launch_field_slab(pn_context *c, int slot, const double *src, double *dst, cudaStream_t s, int src_k0,
+                      int src_nk) {
     const Geo &g = c->g;
     int nplanes = g.nzl + 1;
+    if (src_nk <= 0) { src_k0 = 0; src_nk = g.nz; }   // the global field
     dim3 grid((g.nx + 31) / 32, (nplanes + 31) / 32, g.ny), block(32, 8);
-    k_field_slab<<<grid, block, 0, s>>>(src, dst, g.nx, g.ny, g.nz, g.z0, nplanes);
+    k_field_slab<<<grid, block, 0, s>>>(src, dst, g.nx, g.ny, g.nz, g.z0, nplanes, src_k0, src_nk);
     PN_CUDA(cudaGetLastError());
     return PN_OK;
 }
@@ -64,6 +66,22 @@ int launch_field_slab(pn_context *c, int slot, const double *src, double *dst, c
 __global__ void k_fill(double *p, long long n, double v) {
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
         p[i] = v;
+}
+
+__global__ void k_fill_hash(double *p, long long n, long long offset, unsigned long long seed) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        unsigned long long z = seed + 0x9E3779B97F4A7C15ULL * (unsigned long long)(offset + i + 1);   // splitmix64
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+        z ^= z >> 31;
+        p[i] = (double)(z >> 11) * 0x1.0p-52 - 1.0;
+    }
+}
+
+int launch_fill_hash(double *p, long long n, long long offset, unsigned long long seed, cudaStream_t s) {
+    k_fill_hash<<<1184, 256, 0, s>>>(p, n, offset, seed);
+    PN_CUDA(cudaGetLastError());
+    return PN_OK;
 }
 
 int launch_fill(double *p, long long n, double v, cudaStream_t s) {
@@ -1114,6 +1132,9 @@ __global__ void __launch_bounds__(256, 4) k_cg_small(Tables T, Fields F, Geo g, 
 int cg_small_capacity(pn_context *c, long long *rows) {
     auto kern = k_cg_small<false>;   // the solve assembles the stored diagonal first
     const size_t sm = small_smem(c);
+    int optin = 0;
+    PN_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
+    if (sm > (size_t)optin) { *rows = 0; return PN_OK; }   // tables do not fit: the chain runs instead
     if (sm > 48 * 1024) PN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     int per_sm = 0, nsm = 0;
     PN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, sm));

@@ -87,6 +87,16 @@ struct SegActive {
     }
 };
 
+// The replayed iteration graph holds kernel arguments by value (vector and
+// history pointers, the segmented operator's __grid_constant__ parameters with
+// lambda_l p_l): anything that changes them drops the graph.
+static void drop_graph(pn_context *c) {
+    if (c->gexec) cudaGraphExecDestroy(c->gexec);
+    c->gexec = nullptr;
+    c->gkey = -1;
+    ++c->gen;   // a group graph held by another context sees this too
+}
+
 static int ensure_diag(pn_context *c, cudaStream_t s) {
     if (c->diag_ready) return PN_OK;
     PN_TRY(launch_setup(c, true, false, s));
@@ -213,6 +223,14 @@ int pn_create(const pn_desc *d, pn_context **out) {
     c->h_lidx.assign(d->lidx, d->lidx + d->U);
     c->h_aw.assign(d->a_w, d->a_w + d->n_a);
     c->h_tw.assign(d->t_w, d->t_w + d->n_t);
+    c->h_aptr.assign(d->a_ptr, d->a_ptr + d->U + 1);
+    c->h_atgt.assign(d->a_tgt, d->a_tgt + d->n_a);
+    c->h_adir.assign(d->a_dir, d->a_dir + d->n_a);
+    c->h_adiag.assign(d->a_diag, d->a_diag + d->n_a);
+    c->h_tptr.assign(d->t_ptr, d->t_ptr + d->U + 1);
+    c->h_tsrc.assign(d->t_src, d->t_src + d->n_t);
+    c->h_tdir.assign(d->t_dir, d->t_dir + d->n_t);
+    c->h_tdiag.assign(d->t_diag, d->t_diag + d->n_t);
     c->h_rptr.assign(d->r_ptr, d->r_ptr + d->U + 1);
     c->h_hascoef.assign(d->term_hascoef, d->term_hascoef + d->n_terms);
     c->h_nf.assign(d->term_nf, d->term_nf + d->n_terms);
@@ -497,11 +515,21 @@ int pn_destroy(pn_context *c) {
     return PN_OK;
 }
 
-int pn_set_field(pn_context *c, int32_t slot, int32_t kind, double scalar, const double *data, void *stream) {
+static int set_field_impl(pn_context *c, int32_t slot, int32_t kind, double scalar, const double *data, int32_t k0,
+                          int32_t nk, void *stream) {
     if (c && c->is_csr) { set_error("not available for a generic CSR system"); return PN_ERR_UNSUPPORTED; }
     if (!c || slot < 0 || slot >= c->n_fields) { set_error("bad field slot"); return PN_ERR_INVALID; }
+    if (kind < 0 || kind > 2) { set_error("bad field kind"); return PN_ERR_INVALID; }
+    if (nk > 0) {   // the planes given must cover the slab and its +1 plane (clamped at nz)
+        const long long need_hi = std::min<long long>(c->g.z0 + c->g.nzl + 1, c->g.nz);
+        if (k0 < 0 || k0 > c->g.z0 || (long long)k0 + nk < need_hi || (long long)k0 + nk > c->g.nz) {
+            set_error("field planes do not cover this slab (z0 .. z0 + nz_local, +1 plane)");
+            return PN_ERR_INVALID;
+        }
+    }
     cudaStream_t s = (cudaStream_t)stream;
     PN_CUDA(cudaSetDevice(c->device));
+    drop_graph(c);
     c->f.kind[slot] = kind;
     c->f.scalar[slot] = scalar;
     c->f.data[slot] = nullptr;
@@ -516,7 +544,7 @@ int pn_set_field(pn_context *c, int32_t slot, int32_t kind, double scalar, const
             if (e != cudaSuccess) { dst = nullptr; set_error(cudaGetErrorString(e)); return PN_ERR_NOMEM; }
         }
         if (kind == 1) PN_TRY(launch_fill(dst, (long long)n, scalar, s));   // sigma read as arrays by fast kernels
-        else PN_TRY(launch_field_slab(c, slot, data, dst, s));
+        else PN_TRY(launch_field_slab(c, slot, data, dst, s, k0, nk));
         c->f.kind[slot] = 2;
         c->f.data[slot] = dst;
     }
@@ -525,10 +553,21 @@ int pn_set_field(pn_context *c, int32_t slot, int32_t kind, double scalar, const
     return PN_OK;
 }
 
+int pn_set_field(pn_context *c, int32_t slot, int32_t kind, double scalar, const double *data, void *stream) {
+    return set_field_impl(c, slot, kind, scalar, data, 0, 0, stream);
+}
+
+int pn_set_field_planes(pn_context *c, int32_t slot, int32_t kind, double scalar, const double *data, int32_t k0,
+                        int32_t nk, void *stream) {
+    if (nk < 1) { set_error("n_planes must be >= 1"); return PN_ERR_INVALID; }
+    return set_field_impl(c, slot, kind, scalar, data, k0, nk, stream);
+}
+
 int pn_setup(pn_context *c, void *stream) {
     if (c && c->is_csr) { set_error("not available for a generic CSR system"); return PN_ERR_UNSUPPORTED; }
     cudaStream_t s = (cudaStream_t)stream;
     PN_CUDA(cudaSetDevice(c->device));
+    drop_graph(c);
     // lambda_l * p_l per comp when every phase field is uniform (fast diagonal)
     c->uniform_phase = 1;
     std::vector<double> lamp(c->U, 0.0);
@@ -726,13 +765,17 @@ static int iteration(std::vector<pn_context *> &cs, const pn_solve_opts *o, bool
 
 // Capture `gb` iterations once per (mode, jacobi, layout) on a private stream
 // and replay the graph until the device stop flag is set.
-static int run_graph_batches(pn_context *c, const pn_solve_opts *o, bool jacobi, bool seg, cudaStream_t s) {
-    std::vector<pn_context *> cs{c};
-    const long long per_it = 8;   // rough launches per iteration, to size batches
+// Slab groups capture their whole iteration too: the NCCL halo send/recv and
+// plane-sum all-gathers on the exchange stream fork from and join back into
+// the capture stream (NCCL records its kernels into the graph), the loopback
+// group's device copies likewise.  One graph per group, held by cs[0].
+static int run_graph_batches(std::vector<pn_context *> &cs, const pn_solve_opts *o, bool jacobi, bool seg,
+                             cudaStream_t s) {
+    pn_context *c = cs[0];
     const long long gb = o->check_every > 0 ? o->check_every : (c->R_l() < (1LL << 22) ? 16 : 4);
-    (void)per_it;
     const long long key = ((long long)o->mode << 40) | ((long long)jacobi << 39) | ((long long)seg << 38) |
-                          ((long long)o->blas_threads << 20) | ((long long)o->blas_kernel << 16) | gb;
+                          ((long long)o->blas_threads << 20) | ((long long)o->blas_kernel << 16) |
+                          ((long long)cs.size() << 8) | gb;
     if (!c->gstream) {
         PN_CUDA(cudaStreamCreateWithFlags(&c->gstream, cudaStreamNonBlocking));
         PN_CUDA(cudaEventCreateWithFlags(&c->gev0, cudaEventDisableTiming));
@@ -741,11 +784,14 @@ static int run_graph_batches(pn_context *c, const pn_solve_opts *o, bool jacobi,
     cudaStream_t g = c->gstream;
     PN_CUDA(cudaEventRecord(c->gev0, s));
     PN_CUDA(cudaStreamWaitEvent(g, c->gev0, 0));
-    if (c->gkey != key || !c->gexec) {
+    std::vector<std::pair<pn_context *, long long>> members;
+    for (auto *m : cs) members.emplace_back(m, m->gen);
+    if (c->gkey != key || !c->gexec || c->gmembers != members) {
         if (c->gexec) { cudaGraphExecDestroy(c->gexec); c->gexec = nullptr; }
         cudaGraph_t graph;
         const long long l0 = c->launches;
-        PN_CUDA(cudaStreamBeginCapture(g, cudaStreamCaptureModeThreadLocal));
+        // relaxed: NCCL may touch its own resources while enqueueing
+        PN_CUDA(cudaStreamBeginCapture(g, c->world > 1 ? cudaStreamCaptureModeRelaxed : cudaStreamCaptureModeThreadLocal));
         int st = PN_OK;
         for (long long k = 0; k < gb && st == PN_OK; ++k) st = iteration(cs, o, jacobi, seg, g);
         cudaError_t e = cudaStreamEndCapture(g, &graph);
@@ -756,6 +802,7 @@ static int run_graph_batches(pn_context *c, const pn_solve_opts *o, bool jacobi,
         c->graph_launches = c->launches - l0;
         c->launches = l0;
         c->gkey = key;
+        c->gmembers = members;
     }
     long long issued = 0;
     while (true) {
@@ -796,7 +843,7 @@ static bool use_small(const std::vector<pn_context *> &cs, const pn_solve_opts *
     if (c->world > 1 || c->is_csr || c->g.nzl != c->g.nz || c->R_l() >= (1LL << 31)) return false;
     if (const char *e = getenv("PNRTE_SMALL_MAX")) return c->R_l() <= atoll(e);
     long long cap = 0;
-    if (cg_small_capacity(c, &cap) != PN_OK) return false;
+    if (cg_small_capacity(c, &cap) != PN_OK) { cudaGetLastError(); return false; }
     if (!pn_seg_ok(c)) return c->R_l() <= cap;
     const long long entries = c->R_l() / c->U * c->tb.n_a;
     return c->R_l() <= 2 * cap && entries <= (c->U > 16 ? (1LL << 21) : (1LL << 20));
@@ -824,6 +871,7 @@ static int solve_group(std::vector<pn_context *> &cs, const pn_solve_opts *o, co
         PN_TRY(alloc_buf(c, c->bs));
         long long hl = std::max<long long>(1, std::min<long long>(o->max_iter, 1LL << 24));
         if (hl > c->hist_len) {
+            drop_graph(c);   // the captured scalar kernels write the old history buffers
             PN_TRY(dalloc(c, &c->hist_n, hl));
             PN_TRY(dalloc(c, &c->hist_p, hl));
             c->hist_len = hl;
@@ -883,16 +931,16 @@ static int solve_group(std::vector<pn_context *> &cs, const pn_solve_opts *o, co
     // Single-context solves replay a captured CUDA graph of `gb` iterations
     // (kernels past the stop are predicated no-ops).
     if (o->max_iter > 0) {
-        const bool graph = cs.size() == 1 && c0->world <= 1 && o->check_every >= 0;
+        const bool graph = o->check_every >= 0;
         if (small) {
             PN_TRY(ensure_diag(c0, s));   // one load per row instead of up to 16 site samples
             if (!c0->small_parts) PN_TRY(dalloc(c0, &c0->small_parts, (size_t)4 * SMALL_MAX_BLOCKS));
             if (!c0->small_vecs) PN_TRY(dalloc(c0, &c0->small_vecs, (size_t)2 * c0->R_l()));
             const int st = launch_cg_small(c0, jacobi, s);
-            if (st == PN_ERR_UNSUPPORTED) PN_TRY(run_graph_batches(c0, o, jacobi, false, s));
+            if (st == PN_ERR_UNSUPPORTED) PN_TRY(run_graph_batches(cs, o, jacobi, false, s));
             else if (st != PN_OK) return st;
         } else if (graph) {
-            PN_TRY(run_graph_batches(c0, o, jacobi, seg, s));
+            PN_TRY(run_graph_batches(cs, o, jacobi, seg, s));
         } else {
             long long batch = o->check_every > 0 ? o->check_every : 4;
             long long issued = 0;
@@ -1045,12 +1093,16 @@ int pn_bench(pn_context *c, int32_t what, int32_t reps, double *ms_per, void *st
     o.tol = 1e-300;
     o.max_iter = 1LL << 40;
     o.mode = 0;
-    // deterministic non-trivial inputs: p = r = b (solve layout), once
+    // dense deterministic inputs (uniform [-1, 1) by global index; the RHS of
+    // a point-source problem is almost all zeros), converted to the solve layout
     if (!c->bench_ready) {
-        PN_TRY(alloc_buf(c, c->bs));
-        PN_TRY(to_solve_layout(c, seg, c->b.p, c->bs.p, s));
-        PN_TRY(group_vec(cs, V_COPY, &pn_context::p, &pn_context::bs, nullptr, false, s));
-        PN_TRY(group_vec(cs, V_COPY, &pn_context::r, &pn_context::bs, nullptr, false, s));
+        const long long off = (long long)c->g.z0 * c->g.plane;
+        PN_TRY(launch_fill_hash(c->tmp.p, c->R_l(), off, 0x5EEDULL, s));
+        PN_TRY(to_solve_layout(c, seg, c->tmp.p, c->p.p, s));
+        PN_TRY(launch_fill_hash(c->tmp.p, c->R_l(), off, 0xF00DULL, s));
+        PN_TRY(to_solve_layout(c, seg, c->tmp.p, c->r.p, s));
+        PN_TRY(launch_fill_hash(c->tmp.p, c->R_l(), off, 0xBEEFULL, s));
+        PN_TRY(to_solve_layout(c, seg, c->tmp.p, c->z.p, s));
         c->bench_ready = true;
     }
     if (what == 1 || what == 3 || what == 4 || what == 5) {

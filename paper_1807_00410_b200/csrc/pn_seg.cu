@@ -47,6 +47,37 @@ __global__ void k_sig_pad(const double *__restrict__ src, double *__restrict__ d
     }
 }
 
+// The generated code hard-wires the stencil structure of build_tables(N): every
+// table entry must match it (target / source comp, direction, diagonal flag,
+// |w| class and sign), otherwise the table operator runs instead.
+static bool seg_structure_ok(const pn_context *c) {
+    if ((int)c->h_par.size() != c->U) return false;
+    for (int trans = 0; trans < 2; ++trans) {
+        const int *sig = seg_sig(c->N, trans);
+        int nw = 0;
+        const int *rep = seg_wrep(c->N, trans, &nw);
+        if (!sig || !rep || sig[0] != c->U) return false;
+        const int U = sig[0], n = sig[1];
+        const int *ptr = sig + 2, *oth = ptr + U + 1, *dir = oth + n, *dg = dir + n, *code = dg + n, *par = code + n;
+        const std::vector<int> &hp = trans ? c->h_tptr : c->h_aptr, &ho = trans ? c->h_tsrc : c->h_atgt,
+                               &hd = trans ? c->h_tdir : c->h_adir, &hg = trans ? c->h_tdiag : c->h_adiag;
+        const std::vector<double> &hw = trans ? c->h_tw : c->h_aw;
+        if ((int)ho.size() != n || (int)hw.size() != n || (int)hp.size() != U + 1) return false;
+        for (int q = 0; q <= U; ++q)
+            if (hp[q] != ptr[q]) return false;
+        for (int q = 0; q < U; ++q)
+            if (c->h_par[q] != par[q]) return false;
+        for (int e = 0; e < n; ++e) {
+            if (ho[e] != oth[e] || hd[e] != dir[e] || (hg[e] != 0) != (dg[e] != 0)) return false;
+            if (dg[e]) continue;
+            const int u = code[e] >> 1, neg = code[e] & 1;
+            if (u >= nw || rep[u] >= n) return false;
+            if (std::fabs(hw[e]) != std::fabs(hw[rep[u]]) || (int)std::signbit(hw[e]) != neg || hw[e] == 0.0) return false;
+        }
+    }
+    return true;
+}
+
 bool pn_seg_ok(const pn_context *c) { return c->seg && ((SegCtx *)c->seg)->ok; }
 
 int pn_seg_prepare(pn_context *c, cudaStream_t s) {
@@ -58,6 +89,7 @@ int pn_seg_prepare(pn_context *c, cudaStream_t s) {
     sc->ok = false;
     if (!seg_geometry_ok(c) || !c->uniform_phase || c->red_bx < pn_seg_red_blocks(c)) return PN_OK;
     if (c->f.kind[0] != 2 || c->f.kind[1] != 2) return PN_OK;   // sigma arrays (uniform ones are materialised)
+    if (!seg_structure_ok(c)) return PN_OK;
     if (!sc->pa) {
         sc->pa = new SegParams();
         sc->pt = new SegParams();

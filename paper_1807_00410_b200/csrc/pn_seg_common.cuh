@@ -14,6 +14,7 @@
 // last face of its staggered axis reads as 0 off the diagonal, and a pinned
 // row keeps only diag * x.
 #pragma once
+#include <atomic>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -466,12 +467,17 @@ int seg_launch(const SegParams &prm, const SegGeo &g0, int trans, int red, bool 
     dim3 grid((unsigned)nblk), block(SegTune<N>::threads);
     const size_t smem = rows * seg_smem_per_warp<N>();
     if (g.nyb != (g.ny + rows - 1) / rows) { set_error("segmented launch: row blocking mismatch"); return PN_ERR_INVALID; }
+    int dev = 0;
+    PN_CUDA(cudaGetDevice(&dev));
 #define PN_SEG_GO3(T, R, J, B, P)                                                                                 \
     do {                                                                                                          \
-        static bool cfg_done = false;                                                                             \
-        if (!cfg_done) {                                                                                          \
-            cudaFuncSetAttribute(k_seg<N, T, R, J, B, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-            cfg_done = true;                                                                                      \
+        /* the attribute is per device: one bit per device ordinal */                                           \
+        static std::atomic<unsigned long long> cfg_mask{0};                                                       \
+        const unsigned long long bit_ = 1ULL << (dev & 63);                                                       \
+        if (!(cfg_mask.load() & bit_)) {                                                                          \
+            PN_CUDA(cudaFuncSetAttribute(k_seg<N, T, R, J, B, P>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
+                                         (int)smem));                                                             \
+            cfg_mask.fetch_or(bit_);                                                                              \
         }                                                                                                         \
         k_seg<N, T, R, J, B, P><<<grid, block, smem, s>>>(prm, g, x, y, minv, zt, st, ss, partials, slot_stride,  \
                                                           rb, state);                                             \

@@ -33,6 +33,16 @@ class ProblemSpec:
     bc: str = "dirichlet"
     sigma_t_floor: float = 0.0
     name: str = ""
+    # (k0, n_planes): the array fields hold only the global z-planes
+    # [k0, k0 + n_planes) (shape (nx, ny, n_planes)) -- one rank's share of a
+    # slab decomposition (configs.make_config(..., planes=)); None = whole grid
+    z_planes: tuple | None = None
+
+    @property
+    def field_shape(self):
+        if self.z_planes is None:
+            return tuple(self.res)
+        return (self.res[0], self.res[1], int(self.z_planes[1]))
 
     def __post_init__(self):
         hs = {self.extent[k] / self.res[k] for k in range(self.dim)}
@@ -54,10 +64,10 @@ class ProblemSpec:
         if name in self.fields:
             arr = self.fields[name]
             if np.ndim(arr) == 0:
-                return np.full(self.res, float(arr))
+                return np.full(self.field_shape, float(arr))
             return arr
         if name.startswith("p_") or name.startswith("Q_"):
-            return np.zeros(self.res)
+            return np.zeros(self.field_shape)
         raise KeyError(f"unknown parameter field {name!r}")
 
     def centers(self, axis):
@@ -109,8 +119,9 @@ def field_slot(spec, name):
         if np.ndim(arr) == 0:
             return 1, float(arr), None
         arr = np.asarray(arr, dtype=np.float64)
-        if tuple(arr.shape) != tuple(spec.res):
-            raise ValueError(f"field {name!r} has shape {arr.shape}, expected {tuple(spec.res)}")
+        want = tuple(getattr(spec, "field_shape", spec.res))
+        if tuple(arr.shape) != want:
+            raise ValueError(f"field {name!r} has shape {arr.shape}, expected {want}")
         return 2, 0.0, arr
     if fields is None:
         arr = np.asarray(spec.field_array(name), dtype=np.float64)

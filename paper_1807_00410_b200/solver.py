@@ -70,18 +70,32 @@ def _stream(torch):
     return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
+class BlasConfigError(RuntimeError):
+    """Faithful mode cannot tell which OpenBLAS ddot to reproduce."""
+
+
 def blas_config():
     """(threads, kernel) of this process's OpenBLAS, which the reference's
-    numpy uses; kernel 0 = SkylakeX, 1 = Haswell."""
+    numpy uses; kernel 0 = SkylakeX, 1 = Haswell.  Raises BlasConfigError
+    when threadpoolctl cannot find an OpenBLAS with a known ddot kernel
+    (faithful solves then need blas_threads / blas_kernel given explicitly)."""
     try:
         from threadpoolctl import threadpool_info
-        for info in threadpool_info():
-            if info.get("internal_api") == "openblas":
-                arch = (info.get("architecture") or "").lower()
-                return int(info["num_threads"]), (1 if arch in ("haswell", "zen") else 0)
-    except Exception:
-        pass
-    return 8, 0
+        infos = threadpool_info()
+    except Exception as e:   # threadpoolctl missing or broken
+        raise BlasConfigError(f"cannot query the OpenBLAS configuration ({e}); "
+                              "pass blas_threads and blas_kernel") from None
+    for info in infos:
+        if info.get("internal_api") == "openblas":
+            arch = (info.get("architecture") or "").lower()
+            if arch in ("haswell", "zen"):
+                return int(info["num_threads"]), 1
+            if arch == "skylakex":
+                return int(info["num_threads"]), 0
+            raise BlasConfigError(f"OpenBLAS ddot kernel {arch!r} has no emulation; "
+                                  "pass blas_threads and blas_kernel")
+    raise BlasConfigError("no OpenBLAS in this process (faithful mode reproduces the reference's "
+                          "OpenBLAS ddot); pass blas_threads and blas_kernel")
 
 
 class PnContext:
@@ -224,20 +238,28 @@ class PnContext:
         return self._torch.device("cuda", self.device)
 
     def set_fields(self, spec):
-        """Upload every field slot (reference [i,j,k] C-order arrays)."""
+        """Upload every field slot (reference [i,j,k] C-order arrays).  A spec
+        with ``z_planes = (k0, n)`` carries only those global planes (one
+        rank's share, covering its slab and the +1 plane)."""
         torch = self._torch
         held = []
+        zp = getattr(spec, "z_planes", None)
+        shape = self.res if zp is None else (self.res[0], self.res[1], int(zp[1]))
         with torch.cuda.device(self.device):
             s = _stream(torch)
             for slot, name in enumerate(field_slots(self.tables)):
                 kind, scal, arr = field_slot(spec, name)
                 ptr = None
                 if kind == 2:
-                    arr = np.asarray(arr, dtype=np.float64).reshape(self.res)   # 2-D fields: [i, j] -> [i, j, 1]
+                    arr = np.asarray(arr, dtype=np.float64).reshape(shape)   # 2-D fields: [i, j] -> [i, j, 1]
                     t = torch.from_numpy(np.ascontiguousarray(arr)).to(self.dev, non_blocking=False)
                     held.append(t)
                     ptr = ctypes.c_void_p(t.data_ptr())
-                _lib.check(self._L.pn_set_field(self.handle, slot, kind, scal, ptr, s))
+                if zp is None:
+                    _lib.check(self._L.pn_set_field(self.handle, slot, kind, scal, ptr, s))
+                else:
+                    _lib.check(self._L.pn_set_field_planes(self.handle, slot, kind, scal, ptr, int(zp[0]),
+                                                           int(zp[1]), s))
             _lib.check(self._L.pn_setup(self.handle, s))
             torch.cuda.current_stream().synchronize()
         del held
@@ -279,7 +301,7 @@ class PnContext:
         o.mode = 1 if mode == "faithful" else 0
         # the OpenBLAS configuration matters to the faithful mode only (its ddot
         # emulation); querying it scans the loaded libraries (~0.5 ms per call)
-        th, kn = (8, 0)
+        th, kn = (1, 0)   # unused by fast solves
         if o.mode == 1 and (blas_threads is None or blas_kernel is None):
             th, kn = blas_config()
         o.blas_threads = int(blas_threads if blas_threads is not None else th)

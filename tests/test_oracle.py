@@ -151,3 +151,36 @@ def test_oracle_neumann_matches_live_reference(ref):
     s = assemble(compile_program(build_pn(4, 3)), spec)
     A = StencilOracle(build_tables(4), spec).csr()
     assert np.array_equal(A.indices, s.A.indices) and A.data.tobytes() == s.A.data.tobytes()
+
+
+@pytest.mark.parametrize("idx", [3, 4])
+def test_oracle_perfcfg_assembly_and_products(idx, golden):
+    """The config-3/4 generators at 32^3 (floor 1): the oracle reproduces the
+    live reference's assembly and products (tests/golden/perfcfg.json)."""
+    import json
+    from paper_1807_00410_b200.configs import solve_spec
+    want = json.loads((golden["dir"] / "perfcfg.json").read_text())[f"cfg{idx}_n32"]
+    cfg = make_config(idx, n=32)
+    o = StencilOracle(build_tables(cfg.N), solve_spec(cfg))
+    A = o.csr()
+    assert sha(A.indices.astype(np.int32)) == want["A_indices_sha256"]
+    assert sha(A.data) == want["A_data_sha256"]
+    assert sha(o.rhs) == want["Q_sha256"]
+    x = probe_vector(o.R)
+    assert sha(o.apply(x)) == want["Ax_sha256"]
+    assert sha(o.apply(x, True)) == want["Atx_sha256"]
+
+
+def test_oracle_perfcfg3_solve_matches_reference(golden):
+    """The whole config-3-generator CGNR at 32^3 (452 iterations to 1e-6): the
+    oracle's trajectory is the reference's, bit for bit."""
+    import json
+    from paper_1807_00410_b200.configs import solve_spec
+    want = json.loads((golden["dir"] / "perfcfg.json").read_text())["cfg3_n32"]
+    cfg = make_config(3, n=32)
+    o = StencilOracle(build_tables(cfg.N), solve_spec(cfg))
+    x, rep = o.cgnr(tol=cfg.tol, max_iter=cfg.max_iter, blas_threads=FIX_BLAS[0], blas_kernel=FIX_BLAS[1])
+    assert rep["iterations"] == want["iterations"]
+    assert sha(x) == want["x_sha256"]
+    assert rep["normal_history"] == want["normal_history"]
+    assert sha(o.unstagger(x)) == want["unstagger_sha256"]

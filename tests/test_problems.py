@@ -66,3 +66,20 @@ def test_checkerboard_generator_bit_identical(n, ref):
     assert a.res == b.res and a.extent == b.extent and a.dim == b.dim == 2
     for k in b.fields:
         assert np.asarray(a.fields[k]).tobytes() == np.asarray(b.fields[k]).tobytes(), k
+
+
+@pytest.mark.parametrize("idx,n", [(3, 32), (4, 32), (5, 24)])
+def test_slab_generation_equals_planes_of_the_grid(idx, n):
+    """configs.make_config(..., planes=(k0, k1)) generates exactly the global
+    z-planes [k0, k1) of every field (one rank's share of a slab run)."""
+    from paper_1807_00410_b200.configs import make_config
+    full = make_config(idx, n=n)
+    for k0, k1 in ((0, 5), (3, 17), (n - 6, n), (0, n)):
+        part = make_config(idx, n=n, planes=(k0, k1))
+        assert part.spec.z_planes == (k0, k1 - k0)
+        for name, v in full.spec.fields.items():
+            w = part.spec.fields[name]
+            if np.ndim(v) == 0:
+                assert w == v
+            else:
+                assert np.ascontiguousarray(np.asarray(v)[:, :, k0:k1]).tobytes() == np.ascontiguousarray(w).tobytes()

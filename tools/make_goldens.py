@@ -13,6 +13,10 @@ Writes
                        CSR A, Q, CGNR x / histories, unstagger (python tools/make_goldens.py --cda-only)
   configs.json         reference solves of configs 1 and 2: iteration count, sha256
                        of the solution bits, histories, residuals; input hashes
+  perfcfg.json         reference solves of the config-3 and config-4 generators at 32^3
+                       (sigma_t floor tau = 1, tol 1e-6): iteration count, sha256 of x,
+                       Q, A, A@probe, A.T@probe, histories, residuals
+                       (python tools/make_goldens.py --perfcfg-only)
 The numpy/OpenBLAS configuration used is recorded (blas threads and kernel):
 faithful-mode GPU runs must emulate that configuration to be bit-identical.
 """
@@ -111,7 +115,37 @@ def cda():
     (GOLD / "cda.json").write_text(json.dumps(meta, indent=1))
 
 
+def perfcfg():
+    """Reduced-size stand-ins of the performance configs, solved by the live
+    reference exactly as configs.solve_spec sets them up (floor tau = 1)."""
+    from paper_1807_00410_b200.configs import solve_spec
+    out = {"blas": blas()}
+    for idx, n in ((3, 32), (4, 32)):
+        cfg = make_config(idx, n=n)
+        spec = solve_spec(cfg)
+        prog = compile_program(build_pn(cfg.N, 3))
+        sysm = assemble(prog, spec)
+        A = sysm.A
+        x = probe_vector(A.shape[0])
+        xs, rep = solve_normal_cg(sysm, tol=cfg.tol, max_iter=cfg.max_iter)
+        out[f"cfg{idx}_n{n}"] = {
+            "N": cfg.N, "res": list(spec.res), "tol": cfg.tol, "sigma_t_floor": cfg.floor,
+            "iterations": rep.iterations, "converged": rep.converged,
+            "normal_residual": rep.normal_residual, "primal_residual": rep.primal_residual,
+            "x_sha256": sha(xs), "x_norm": float(np.linalg.norm(xs)), "Q_sha256": sha(sysm.Q),
+            "A_data_sha256": sha(A.data), "A_indices_sha256": sha(A.indices.astype(np.int32)),
+            "Ax_sha256": sha(A @ x), "Atx_sha256": sha(A.T.tocsr() @ x),
+            "unstagger_sha256": sha(unstagger(xs, prog, spec.res)),
+            "normal_history": rep.normal_history, "primal_history": rep.primal_history,
+        }
+        print(f"cfg{idx}_n{n}", rep.iterations, sha(xs)[:16], flush=True)
+    (GOLD / "perfcfg.json").write_text(json.dumps(out, indent=1))
+
+
 def main():
+    if "--perfcfg-only" in sys.argv:
+        perfcfg()
+        return
     if "--neumann-only" in sys.argv:
         neumann()
         return
