@@ -64,31 +64,41 @@ def _zrange(n, planes):
     return k0, k1
 
 
+def _shape3(n):
+    return (int(n),) * 3 if np.ndim(n) == 0 else tuple(int(v) for v in n)
+
+
 def value_noise(rng, n, cells, planes=None):
     """Trilinear interpolation of a seeded (cells+1)^3 lattice, the pattern of
-    problems.py:178-192 (z-planes [k0, k1) only when ``planes`` is given)."""
-    k0, k1 = _zrange(n, planes)
-    lattice = rng.random((cells + 1,) * 3)
-    t = np.linspace(0.0, cells, n, endpoint=False)
-    i0 = np.floor(t).astype(int)
-    frac = t - i0
-    i1 = np.minimum(i0 + 1, cells)
-    out = np.zeros((n, n, k1 - k0))
-    fx, fy, fz = frac[:, None, None], frac[None, :, None], frac[None, None, k0:k1]
-    for dx, wx in ((i0, 1 - fx), (i1, fx)):
-        for dy, wy in ((i0, 1 - fy), (i1, fy)):
-            for dz, wz in ((i0[k0:k1], 1 - fz), (i1[k0:k1], fz)):
+    problems.py:178-192 (z-planes [k0, k1) only when ``planes`` is given).
+    ``n`` / ``cells`` may be per-axis triples (box grids of the weak-scaling
+    workload); scalars give the cubic configs."""
+    shape, cl = _shape3(n), _shape3(cells)
+    k0, k1 = _zrange(shape[2], planes)
+    lattice = rng.random(tuple(c + 1 for c in cl))
+    ax = []
+    for m, c in zip(shape, cl):
+        t = np.linspace(0.0, c, m, endpoint=False)
+        i0 = np.floor(t).astype(int)
+        ax.append((i0, t - i0, np.minimum(i0 + 1, c)))
+    (ix0, frx, ix1), (iy0, fry, iy1), (iz0, frz, iz1) = ax
+    out = np.zeros((shape[0], shape[1], k1 - k0))
+    fx, fy, fz = frx[:, None, None], fry[None, :, None], frz[None, None, k0:k1]
+    for dx, wx in ((ix0, 1 - fx), (ix1, fx)):
+        for dy, wy in ((iy0, 1 - fy), (iy1, fy)):
+            for dz, wz in ((iz0[k0:k1], 1 - fz), (iz1[k0:k1], fz)):
                 out += (wx * wy * wz) * lattice[np.ix_(dx, dy, dz)]
     return out
 
 
 def cloud_density(rng, n, base_period, octaves=4, persistence=0.5, cut=0.4, planes=None):
-    k0, k1 = _zrange(n, planes)
+    shape = _shape3(n)
+    k0, k1 = _zrange(shape[2], planes)
     amps = [persistence ** o for o in range(octaves)]
-    noise = np.zeros((n, n, k1 - k0))
+    noise = np.zeros((shape[0], shape[1], k1 - k0))
     for o in range(octaves):
-        cells = max(1, (n * (2 ** o)) // base_period)
-        noise += amps[o] * value_noise(rng, n, cells, planes)
+        cells = tuple(max(1, (m * (2 ** o)) // base_period) for m in shape)
+        noise += amps[o] * value_noise(rng, shape, cells, planes)
     noise /= sum(amps)
     return np.clip((noise - cut) / (1.0 - cut), 0.0, 1.0)
 
@@ -162,6 +172,31 @@ def config5(seed=0, n=512, planes=None):
     c = config3(seed=seed, n=n, base_period=n // 4, planes=planes)
     return Config(5, 5, c.spec, 1e-300, 200, None,
                   f"P5 {n}^3 cfg-3 generator, fixed 200 iterations")
+
+
+def weak_config(k, seed=0, n=256, planes=None):
+    """Weak-scaling companion of config 5: the config-3
+    generator (P5, cloud cut 0.4, sigma_t <= 50, albedo 0.95, g = 0.6, z = 0
+    emission slab) on an (n, n, n k) box with the h of n^3 (h = 2/n), noise
+    base period n/4 -- k GPUs each own one n^3 slab.  Fixed 200 iterations."""
+    N = 5
+    shape = (n, n, n * k)
+    k0, k1 = _zrange(shape[2], planes)
+    rng = np.random.default_rng(seed)
+    st = 50.0 * cloud_density(rng, shape, max(1, n // 4), planes=planes)
+    fields = {"sigma_t": st, "sigma_s": 0.95 * st}
+    pe = phase_fields(0.9, N)
+    for l in range(N + 1):
+        q = np.zeros((n, n, k1 - k0))
+        if k0 == 0:
+            q[:, :, 0] = float(pe[f"p_{l}"])
+        fields[q_name(l, 0)] = q
+    fields.update(phase_fields(0.6, N))
+    zp = None if planes is None else (k0, k1 - k0)
+    h = 2.0 / n
+    spec = ProblemSpec(dim=3, origin=(-1.0,) * 3, extent=(2.0, 2.0, h * n * k), res=shape, fields=fields,
+                       bc="dirichlet", name=f"weak{k}", z_planes=zp)
+    return Config(0, N, spec, 1e-300, 200, None, f"P5 {n}x{n}x{n * k} cfg-3 generator (weak scaling, {k} GPUs)")
 
 
 CONFIGS = {1: config1, 2: config2, 3: config3, 4: config4, 5: config5}

@@ -97,8 +97,16 @@ static void drop_graph(pn_context *c) {
     ++c->gen;   // a group graph held by another context sees this too
 }
 
+// the stored diagonal (R doubles, 8.6 GB at config 4) is allocated on first
+// use: the fast segmented path recomputes it and never needs it
+static int alloc_diag(pn_context *c) {
+    if (!c->diag) PN_TRY(dalloc(c, &c->diag, (size_t)c->R_l()));
+    return PN_OK;
+}
+
 static int ensure_diag(pn_context *c, cudaStream_t s) {
     if (c->diag_ready) return PN_OK;
+    PN_TRY(alloc_diag(c));
     PN_TRY(launch_setup(c, true, false, s));
     c->diag_ready = true;
     return PN_OK;
@@ -275,7 +283,6 @@ int pn_create(const pn_desc *d, pn_context **out) {
     if (st == PN_OK) st = dalloc(c, &c->state, 1);
     if (st == PN_OK) st = dalloc(c, &c->counter, 1);
     if (st == PN_OK && cudaMemset(c->counter, 0, sizeof(unsigned)) != cudaSuccess) st = PN_ERR_CUDA;
-    if (st == PN_OK) st = dalloc(c, &c->diag, (size_t)c->R_l());
     if (st == PN_OK) st = alloc_buf(c, c->b);
     if (st == PN_OK && cudaMallocHost(&c->h_state, sizeof(State)) != cudaSuccess) st = PN_ERR_NOMEM;
     if (st == PN_OK) {
@@ -583,6 +590,7 @@ int pn_setup(pn_context *c, void *stream) {
     // the stored diagonal is only needed by the faithful path (and by the fast
     // path when it cannot recompute the diagonal); it is assembled on demand
     const bool need_diag = !(c->canonical_diag && c->uniform_phase);
+    if (need_diag) PN_TRY(alloc_diag(c));
     PN_TRY(launch_setup(c, need_diag, true, s));
     c->diag_ready = need_diag;
     PN_TRY(pn_seg_prepare(c, s));
@@ -1036,6 +1044,10 @@ int pn_unstagger(pn_context *c, const double *u, double *out, void *stream) {
         return launch_unstagger(c, u, out, (cudaStream_t)stream);
     }
     cudaStream_t s = (cudaStream_t)stream;
+    if (!c || !u || !out) { set_error("invalid arguments"); return PN_ERR_INVALID; }
+    PN_CUDA(cudaSetDevice(c->device));
+    if (c->world <= 1) return launch_unstagger(c, u, out, s);   // one slab reads only its own planes
+    // slabs: the z-staggered comps of plane 0 read plane z0 - 1 (the lower halo)
     PN_TRY(alloc_buf(c, c->tmp));
     PN_CUDA(cudaMemcpyAsync(c->tmp.p, u, c->R_l() * sizeof(double), cudaMemcpyDeviceToDevice, s));
     std::vector<pn_context *> cs{c};

@@ -235,27 +235,31 @@ def transport_couplings(l, m):
     return out
 
 
-def scope(N):
-    return [(l, m) for l in range(N + 1) for m in range(-l, l + 1)]
+def scope(N, dim=3):
+    """(l, m) carried at order N; the 2-D reduction (z-independence) keeps
+    only even l + m (equations.py:51-64)."""
+    return [(l, m) for l in range(N + 1) for m in range(-l, l + 1) if dim == 3 or (l + m) % 2 == 0]
 
 
-def _in_scope(lm, N):
+def _in_scope(lm, N, dim=3):
     l, m = lm
-    return 0 <= l <= N and abs(m) <= l
+    return 0 <= l <= N and abs(m) <= l and (dim == 3 or (l + m) % 2 == 0)
 
 
 # ---------------------------------------------------------------------------
 # restated builder
 # ---------------------------------------------------------------------------
 
-def _placement(N):
+def _placement(N, dim=3):
     """Per-axis parity 2-colouring of the coupling graph seeded by (0,0) at
-    the voxel centre (stencil.py:81-123)."""
-    unknowns = scope(N)
+    the voxel centre (stencil.py:81-123); 2-D drops the z couplings."""
+    unknowns = scope(N, dim)
     edges = []
     for lm in unknowns:
         for axis, tgt, _ in transport_couplings(*lm):
-            if _in_scope(tgt, N):
+            if dim == 2 and axis == 2:
+                continue
+            if _in_scope(tgt, N, dim):
                 par = tuple(1 if k == axis else 0 for k in range(AXES))
                 edges.append((lm, tgt, par))
     off = {unknowns[0]: (0, 0, 0)}
@@ -290,12 +294,24 @@ def _sites(location):
     return sites
 
 
-def build_tables(N):
-    """Tables of compile_program(build_pn(N, 3)) without computer algebra."""
+def comp_index_dim(l, m, N, dim):
+    """Flat unknown index: l(l+1)+m in 3-D, the rank among the even-parity
+    pairs in (l, m) order in 2-D (equations.py:85-103)."""
+    if dim == 3:
+        return comp_index(l, m)
+    return scope(N, 2).index((l, m))
+
+
+def build_tables(N, dim=3):
+    """Tables of compile_program(build_pn(N, dim)) without computer algebra.
+    2-D programs (equations.py:191-210 with dim = 2: odd l + m dropped, no z
+    transport) are embedded as nz = 1 grids: z parity 0, z offsets 0."""
     if N < 1:
         raise InvalidOrderError(f"order must be >= 1, got {N}")
-    unknowns = scope(N)
-    place = _placement(N)
+    if dim not in (2, 3):
+        raise ValueError(f"dim must be 2 or 3, got {dim}")
+    unknowns = scope(N, dim)
+    place = _placement(N, dim)
     rows = []
     for lm in unknowns:
         l, m = lm
@@ -304,7 +320,7 @@ def build_tables(N):
         # coefficient of each sample is Num(+-w) * h^-1 (stencil.py:143-151)
         coeffs = {}
         for axis, tgt, w in transport_couplings(l, m):
-            if not _in_scope(tgt, N):
+            if (dim == 2 and axis == 2) or not _in_scope(tgt, N, dim):
                 continue
             for sgn in (+1, -1):
                 off = tuple(loc[k] + (sgn if k == axis else 0) for k in range(AXES))
@@ -327,14 +343,14 @@ def build_tables(N):
         for (tgt, off), ws in coeffs.items():
             home = place[tgt]
             disp = tuple((off[k] - home[k]) // 2 for k in range(AXES))
-            entries.append(Entry(comp_index(*tgt), tgt, off, disp, False, tuple(ws), ()))
-        entries.append(Entry(comp_index(l, m), lm, loc, (0, 0, 0), True, (), tuple(terms)))
+            entries.append(Entry(comp_index_dim(*tgt, N, dim), tgt, off, disp, False, tuple(ws), ()))
+        entries.append(Entry(comp_index_dim(l, m, N, dim), lm, loc, (0, 0, 0), True, (), tuple(terms)))
         entries.sort(key=lambda e: (e.target_lm, e.offset))
         rc = -1.0 if n == 1 else -1.0 * (1.0 / n)
         rhs = tuple(Term(rc, ((q_name(l, m), s),)) for s in sites)
-        rows.append(Row(comp_index(l, m), lm, loc, tuple(entries), rhs))
+        rows.append(Row(comp_index_dim(l, m, N, dim), lm, loc, tuple(entries), rhs))
     rows.sort(key=lambda r: r.comp)
-    return PnTables(N=N, U=len(rows), rows=tuple(rows))
+    return PnTables(N=N, U=len(rows), rows=tuple(rows), dim=dim)
 
 
 # ---------------------------------------------------------------------------
@@ -433,12 +449,13 @@ def tables_from_program(program):
     return PnTables(N=program.N, U=U, rows=tuple(rows), dim=program.dim)
 
 
-def as_tables(program_or_N):
-    """Accept an order N, our PnTables, or a reference StencilProgram."""
+def as_tables(program_or_N, dim=3):
+    """Accept an order N (with the problem's dim), our PnTables, or a
+    reference StencilProgram."""
     if isinstance(program_or_N, PnTables):
         return program_or_N
     if isinstance(program_or_N, int):
-        return build_tables(program_or_N)
+        return build_tables(program_or_N, dim=dim)
     return tables_from_program(program_or_N)
 
 

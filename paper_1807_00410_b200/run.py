@@ -1,20 +1,17 @@
-"""Device-integrated batch run (the reference's `pnrte run`, cli.py:133-171).
+"""Batch front door with the solve on the GPU (the reference's `pnrte run`,
+cli.py:133-171: problem -> assemble -> CGNR -> unstagger -> artifacts).
 
     python -m paper_1807_00410_b200.run run --problem cfg2 --order 3 --out out/
 
-Same pipeline and artifacts as the reference CLI, with the solve on the GPU:
-build the stencil tables -> assemble on the device -> CGNR -> unstagger ->
-field.pnfld (PNFLD1), profile.csv (fluence along +x through the centre),
-solve.log (residual history).  Exit codes as cli.py:27-30: 0 ok, 2 config
-error, 3 non-convergence or singular system (vacuum) at admission, 4
-internal error.
+Artifacts: field.pnfld (PNFLD1), profile.csv (fluence along +x through the
+centre), solve.log (residual history).  Exit status follows cli.py:27-30:
+0 converged, 2 bad configuration, 3 not converged or vacuum at admission,
+4 internal error.
 
-Problems: `pointsource` (homogeneous medium, unit point emitter,
-problems.py:130-156 restated) and the BASELINE configurations `cfg1`..`cfg5`
+Problems: `pointsource` (homogeneous medium with a unit emitter,
+problems.py:130-156) and the BASELINE configurations `cfg1`..`cfg5`
 (configs.py).  Methods: `pn` (matrix-free P_N stencil) and `cda` (collapsed
-diffusion, field-dependent couplings: explicit device CSR from
-general.py, field order 0 as cli.py:156).  The 2-D checkerboard is not a
-`run` problem here.
+diffusion: explicit device CSR from general.py, field order 0).
 """
 
 from __future__ import annotations
@@ -23,7 +20,7 @@ import argparse
 import math
 import os
 import sys
-from dataclasses import dataclass, fields as dc_fields, replace
+from dataclasses import dataclass, replace
 
 import numpy as np
 
@@ -37,207 +34,203 @@ SQRT_4PI = math.sqrt(4.0 * math.pi)
 
 
 class ConfigError(Exception):
-    pass
+    """A run option with a bad name or value (exit status 2)."""
 
 
-@dataclass
+def _flag(text):
+    word = str(text).strip().lower()
+    if word in ("1", "true", "yes", "on"):
+        return True
+    if word in ("0", "false", "no", "off"):
+        return False
+    raise ValueError(f"not a boolean: {text!r}")
+
+
+# option name -> (parser, default, admissible-value check or None)
+OPTIONS = {
+    "problem": (str, "pointsource", lambda v: v in PROBLEMS),
+    "method": (str, "pn", lambda v: v in ("pn", "cda")),
+    "order": (int, 1, None),
+    "res": (int, 0, lambda v: v >= 0),                   # 0: the problem's default
+    "floor": (float, -1.0, None),                        # <= 0: the problem's default
+    "tol": (float, 1e-8, lambda v: v > 0),
+    "max_iter": (int, 50000, lambda v: v >= 1),
+    "out": (str, "out", None),
+    "seed": (int, 0, None),
+    "jacobi": (_flag, False, None),
+    "mode": (str, "fast", lambda v: v in ("fast", "faithful")),
+    "bc": (str, "", lambda v: v in ("", "dirichlet", "neumann")),   # '': the problem's
+    "device": (int, 0, lambda v: v >= 0),
+}
+
+
+@dataclass(frozen=True)
 class RunConfig:
     problem: str = "pointsource"
-    method: str = "pn"            # pn | cda
+    method: str = "pn"
     order: int = 1
-    res: int = 0                  # 0 = problem default
-    floor: float = -1.0           # < 0 = problem default
+    res: int = 0
+    floor: float = -1.0
     tol: float = 1e-8
     max_iter: int = 50000
     out: str = "out"
     seed: int = 0
     jacobi: bool = False
-    mode: str = "fast"            # fast | faithful
-    bc: str = ""                  # '' = problem default | dirichlet | neumann (cli.py:46,105-107)
+    mode: str = "fast"
+    bc: str = ""
     device: int = 0
-
-    def validated(self):
-        if self.problem not in PROBLEMS:
-            raise ConfigError(f"unknown problem {self.problem!r}")
-        if self.method not in ("pn", "cda"):
-            raise ConfigError(f"unknown method {self.method!r}")
-        if self.method == "pn" and self.order < 1:
-            raise ConfigError(f"order must be >= 1, got {self.order}")
-        if self.tol <= 0:
-            raise ConfigError("tol must be positive")
-        if self.max_iter < 1:
-            raise ConfigError("max-iter must be >= 1")
-        if self.mode not in ("fast", "faithful"):
-            raise ConfigError(f"unknown mode {self.mode!r}")
-        if self.bc and self.bc not in ("dirichlet", "neumann"):
-            raise ConfigError(f"unknown bc {self.bc!r}")
-        return self
-
-
-_BOOLS = {"true": True, "false": False, "1": True, "0": False}
 
 
 def config_from_mapping(mapping):
-    cfg = RunConfig()
-    known = {f.name for f in dc_fields(RunConfig)}
-    for key, val in mapping.items():
-        name = key.replace("-", "_")
-        if name not in known:
-            raise ConfigError(f"unknown config key {key!r}")
-        cur = getattr(cfg, name)
-        if isinstance(cur, bool):
-            if str(val).lower() not in _BOOLS:
-                raise ConfigError(f"bad boolean for {key!r}: {val!r}")
-            setattr(cfg, name, _BOOLS[str(val).lower()])
-        elif isinstance(cur, int):
-            setattr(cfg, name, int(val))
-        elif isinstance(cur, float):
-            setattr(cfg, name, float(val))
-        else:
-            setattr(cfg, name, str(val))
-    return cfg.validated()
+    """RunConfig from string (or typed) values; keys may use '-' or '_'."""
+    values = {}
+    for raw_key, raw in mapping.items():
+        key = str(raw_key).replace("-", "_")
+        if key not in OPTIONS:
+            raise ConfigError(f"unknown option {raw_key!r}")
+        parse, _, ok = OPTIONS[key]
+        try:
+            val = parse(raw)
+        except (TypeError, ValueError) as exc:
+            raise ConfigError(f"option {raw_key!r}: {exc}") from None
+        if ok is not None and not ok(val):
+            raise ConfigError(f"option {raw_key!r}: value {raw!r} not allowed")
+        values[key] = val
+    cfg = RunConfig(**values)
+    if cfg.method == "pn" and cfg.order < 1:
+        raise ConfigError(f"order must be >= 1 for the P_N method, got {cfg.order}")
+    return cfg
 
 
 def make_pointsource(res=80, sigma_t=8.0, albedo=0.9, extent=2.0, g=0.0, max_band=8):
-    """Homogeneous medium with a unit isotropic emitter in the centre voxel,
-    power-preserving 1/(h^3 sqrt(4 pi)) (problems.py:130-156)."""
+    """Homogeneous medium, unit isotropic emitter in the centre voxel with the
+    power-preserving amplitude 1/(h^3 sqrt(4 pi)) (problems.py:130-156)."""
     if res < 8:
         raise ValueError("resolution too small for the point source problem")
     n = int(res)
     h = extent / n
-    shape = (n, n, n)
-    q00 = np.zeros(shape)
-    c = n // 2
-    q00[c, c, c] = 1.0 / (h ** 3 * SQRT_4PI)
-    f = {"sigma_t": np.full(shape, float(sigma_t)), "sigma_s": np.full(shape, float(albedo * sigma_t)),
-         q_name(0, 0): q00}
-    f.update(phase_fields(g, max_band))
-    half = extent / 2.0
-    return ProblemSpec(dim=3, origin=(-half,) * 3, extent=(extent,) * 3, res=shape, fields=f, bc="dirichlet",
-                       sigma_t_floor=min(sigma_t, 1.0), name="pointsource")
+    shape = (n,) * 3
+    emission = np.zeros(shape)
+    emission[(n // 2,) * 3] = 1.0 / (h ** 3 * SQRT_4PI)
+    flds = {"sigma_t": np.full(shape, float(sigma_t)), "sigma_s": np.full(shape, float(albedo * sigma_t)),
+            q_name(0, 0): emission, **phase_fields(g, max_band)}
+    return ProblemSpec(dim=3, origin=(-extent / 2.0,) * 3, extent=(extent,) * 3, res=shape, fields=flds,
+                       bc="dirichlet", sigma_t_floor=min(sigma_t, 1.0), name="pointsource")
 
 
 def build_problem(cfg):
+    """The ProblemSpec a run solves: generator, sigma_t floor, boundary."""
     from .configs import make_config
     if cfg.problem == "pointsource":
-        spec, floor = make_pointsource(cfg.res or 80, max_band=max(8, cfg.order)), None
+        spec, tau = make_pointsource(cfg.res or 80, max_band=max(8, cfg.order)), None
     else:
-        idx = int(cfg.problem[3:])
-        kw = {"seed": cfg.seed}
-        if cfg.res:
-            kw["n"] = cfg.res
-        c = make_config(idx, **kw)
-        spec, floor = c.spec, c.floor
-    tau = cfg.floor if cfg.floor > 0 else floor
-    if tau:
-        spec = floor_sigma_t(spec, tau)
-    if cfg.bc:
-        spec = replace(spec, bc=cfg.bc)
-    return spec
+        kw = {"seed": cfg.seed, **({"n": cfg.res} if cfg.res else {})}
+        made = make_config(int(cfg.problem[len("cfg"):]), **kw)
+        spec, tau = made.spec, made.floor
+    if cfg.floor > 0:
+        tau = cfg.floor
+    spec = floor_sigma_t(spec, tau) if tau else spec
+    return replace(spec, bc=cfg.bc) if cfg.bc else spec
 
 
 def center_profile(spec, coll):
-    """Fluence sqrt(4 pi) L00 along +x through the centre (cli.py:119-130)."""
-    flu = SQRT_4PI * coll[..., 0]
+    """(r, fluence) along +x through the centre line (cli.py:119-130): from
+    the emitter voxel for the point source, across the domain otherwise."""
+    fluence = SQRT_4PI * coll[..., 0]
+    centre = tuple(r // 2 for r in spec.res)
     if spec.name == "pointsource":
-        src = tuple(r // 2 for r in spec.res)
-        line = flu[(slice(src[0], None),) + src[1:]]
-        r = np.arange(line.shape[0]) * spec.h
+        values = fluence[centre[0]:, centre[1], centre[2]]
+        return np.arange(values.shape[0]) * spec.h, values
+    values = fluence[:, centre[1], centre[2]]
+    return spec.centers(0) - spec.origin[0], values
+
+
+def _solve(cfg, spec, log):
+    """Device assembly + CGNR + unstagger; returns (rows, collocated, order, report)."""
+    from .solver import PnContext, assemble_general
+    if cfg.method == "cda":
+        from .general import build_cda_program
+        op, rhs = assemble_general(build_cda_program(spec.dim), spec, device=cfg.device)
+        grid_ctx, order, what = op, 0, "CDA: explicit device CSR, field-dependent couplings"
     else:
-        mid = tuple(r // 2 for r in spec.res)
-        line = flu[(slice(None),) + mid[1:]]
-        r = spec.centers(0) - spec.origin[0]
-    return r, line
+        grid_ctx = PnContext(build_tables(cfg.order, dim=spec.dim), spec.res, spec.h, device=cfg.device)
+        grid_ctx.set_fields(spec)
+        order = cfg.order
+        if spec.bc == "neumann":
+            op, rhs = grid_ctx.assemble_csr("neumann")
+            what = f"P{cfg.order}, Neumann: explicit device CSR"
+        else:
+            op, rhs = grid_ctx, None
+            what = f"matrix-free P{cfg.order} stencil"
+    log(f"assembled {op.R_local} rows on cuda:{cfg.device} ({what})")
+    x, report = op.solve(tol=cfg.tol, max_iter=cfg.max_iter, jacobi=cfg.jacobi, mode=cfg.mode, b=rhs)
+    return op.R_local, grid_ctx.unstagger(x).cpu().numpy(), order, report
+
+
+def _artifacts(cfg, spec, rows, coll, order, report, log):
+    log(f"solve: {report.iterations} iterations, converged={report.converged}, "
+        f"normal={report.normal_residual:.3e}, primal={report.primal_residual:.3e}, wall={report.wall_time:.2f}s")
+    os.makedirs(cfg.out, exist_ok=True)
+    fio.write_field(os.path.join(cfg.out, "field.pnfld"), coll, order)
+    fio.write_profile(os.path.join(cfg.out, "profile.csv"), zip(*center_profile(spec, coll)))
+    summary = {"rows": rows, "method": cfg.method, "mode": cfg.mode, "bc": spec.bc,
+               "iterations": report.iterations, "converged": report.converged,
+               "normal_residual": repr(report.normal_residual), "primal_residual": repr(report.primal_residual),
+               "wall_time": repr(report.wall_time)}
+    history = [f"{k} {n!r} {p!r}" for k, (n, p) in
+               enumerate(zip(report.normal_history, report.primal_history), start=1)]
+    with open(os.path.join(cfg.out, "solve.log"), "w") as fh:
+        fh.write("\n".join([f"{k} {v}" for k, v in summary.items()] + ["# iter normal primal"] + history) + "\n")
 
 
 def run(cfg, log=print):
-    from .solver import PnContext
     spec = build_problem(cfg)
     validate_for_solve(spec)
-    if cfg.method == "cda":
-        return _run_cda(cfg, spec, log)
-    tables = build_tables(cfg.order)
-    os.makedirs(cfg.out, exist_ok=True)
-    ctx = PnContext(tables, spec.res, spec.h, device=cfg.device)
-    ctx.set_fields(spec)
-    R = ctx.R_local
-    if spec.bc == "neumann":
-        op, b = ctx.assemble_csr("neumann")
-        log(f"assembled {R} rows on cuda:{cfg.device} (P{cfg.order}, Neumann: explicit device CSR)")
-    else:
-        op, b = ctx, None
-        log(f"assembled {R} rows on cuda:{cfg.device} (matrix-free P{cfg.order} stencil)")
-    x, report = op.solve(tol=cfg.tol, max_iter=cfg.max_iter, jacobi=cfg.jacobi, mode=cfg.mode, b=b)
-    coll = ctx.unstagger(x).cpu().numpy()
-    _write(cfg, spec, R, coll, cfg.order, report, log)
+    rows, coll, order, report = _solve(cfg, spec, log)
+    _artifacts(cfg, spec, rows, coll, order, report, log)
     return report
 
 
-def _run_cda(cfg, spec, log):
-    from .general import build_cda_program
-    from .solver import assemble_general
-    os.makedirs(cfg.out, exist_ok=True)
-    csr, q = assemble_general(build_cda_program(spec.dim), spec, device=cfg.device)
-    R = csr.R_local
-    log(f"assembled {R} rows on cuda:{cfg.device} (CDA: explicit device CSR, field-dependent couplings)")
-    x, report = csr.solve(tol=cfg.tol, max_iter=cfg.max_iter, jacobi=cfg.jacobi, mode=cfg.mode, b=q)
-    coll = csr.unstagger(x).cpu().numpy()
-    _write(cfg, spec, R, coll, 0, report, log)
-    return report
+# exception class -> (exit status, message prefix), checked in order
+_FAILURES = ((ConfigError, EXIT_CONFIG, "config error"), (InvalidOrderError, EXIT_CONFIG, "config error"),
+             (SingularRiskError, EXIT_NOCONV, "singular system"), (PlacementError, EXIT_INTERNAL, "internal error"),
+             (ValueError, EXIT_CONFIG, "config error"), (OSError, EXIT_CONFIG, "config error"))
 
 
-def _write(cfg, spec, R, coll, order, report, log):
-    log(f"solve: {report.iterations} iterations, converged={report.converged}, "
-        f"normal={report.normal_residual:.3e}, primal={report.primal_residual:.3e}, "
-        f"wall={report.wall_time:.2f}s")
-    fio.write_field(os.path.join(cfg.out, "field.pnfld"), coll, order)
-    r, line = center_profile(spec, coll)
-    fio.write_profile(os.path.join(cfg.out, "profile.csv"), zip(r, line))
-    with open(os.path.join(cfg.out, "solve.log"), "w") as fh:
-        fh.write(f"rows {R}\nmethod {cfg.method}\nmode {cfg.mode}\nbc {spec.bc}\n")
-        fh.write(f"iterations {report.iterations}\nconverged {report.converged}\n")
-        fh.write(f"normal_residual {report.normal_residual!r}\nprimal_residual {report.primal_residual!r}\n")
-        fh.write(f"wall_time {report.wall_time!r}\n# iter normal primal\n")
-        for i, (nr, pr) in enumerate(zip(report.normal_history, report.primal_history), 1):
-            fh.write(f"{i} {nr!r} {pr!r}\n")
-    return report
+def _status(exc):
+    for cls, code, prefix in _FAILURES:
+        if isinstance(exc, cls):
+            print(f"{prefix}: {exc}", file=sys.stderr)
+            return code
+    raise exc
+
+
+def _parser():
+    ap = argparse.ArgumentParser(prog="pnrte-b200", description="B200 P_N solve: run a problem, write artifacts")
+    commands = ap.add_subparsers(dest="command", required=True)
+    p = commands.add_parser("run")
+    p.add_argument("--spec", help="key=value configuration file")
+    for name, (parse, _, _) in OPTIONS.items():
+        flag = "--" + name.replace("_", "-")
+        if parse is _flag:
+            p.add_argument(flag, dest=name, action="store_const", const="true")
+        else:
+            p.add_argument(flag, dest=name)
+    return ap
 
 
 def main(argv=None):
-    parser = argparse.ArgumentParser(prog="pnrte-b200", description="B200 P_N solve: run a problem, export artifacts")
-    sub = parser.add_subparsers(dest="command", required=True)
-    p = sub.add_parser("run")
-    p.add_argument("--spec", help="key=value config file")
-    for f in dc_fields(RunConfig):
-        if f.type in ("bool", bool):
-            p.add_argument("--" + f.name.replace("_", "-"), dest=f.name, action="store_true", default=None)
-        else:
-            p.add_argument("--" + f.name.replace("_", "-"), dest=f.name, default=None)
     try:
-        args = parser.parse_args(argv)
+        args = _parser().parse_args(argv)
     except SystemExit as exc:
-        return EXIT_CONFIG if exc.code not in (0, None) else 0
+        return EXIT_CONFIG if exc.code not in (0, None) else EXIT_OK
     try:
-        mapping = fio.read_config(args.spec) if args.spec else {}
-        for f in dc_fields(RunConfig):
-            v = getattr(args, f.name, None)
-            if v is not None:
-                mapping[f.name] = v
-        cfg = config_from_mapping(mapping)
-    except (ConfigError, ValueError, OSError) as exc:
-        print(f"config error: {exc}", file=sys.stderr)
-        return EXIT_CONFIG
-    try:
+        settings = fio.read_config(args.spec) if args.spec else {}
+        settings.update({k: v for k, v in vars(args).items() if k in OPTIONS and v is not None})
+        cfg = config_from_mapping(settings)
         report = run(cfg)
-    except (InvalidOrderError, ConfigError, ValueError) as exc:
-        print(f"config error: {exc}", file=sys.stderr)
-        return EXIT_CONFIG
-    except SingularRiskError as exc:
-        print(f"singular system: {exc}", file=sys.stderr)
-        return EXIT_NOCONV
-    except PlacementError as exc:
-        print(f"internal error: {exc}", file=sys.stderr)
-        return EXIT_INTERNAL
+    except Exception as exc:   # mapped to the reference's exit statuses
+        return _status(exc)
     if not report.converged:
         print("solver did not converge", file=sys.stderr)
         return EXIT_NOCONV

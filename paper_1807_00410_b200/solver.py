@@ -277,10 +277,12 @@ class PnContext:
                                         _stream(torch)))
         return y
 
-    def diag_rhs(self):
-        d, r = self.empty(), self.empty()
+    def diag_rhs(self, diag=True):
+        """(stored diagonal, RHS Q) as device tensors; diag=False skips the
+        diagonal (the fast path recomputes it and never assembles it)."""
+        d, r = (self.empty() if diag else None), self.empty()
         with self._torch.cuda.device(self.device):
-            _lib.check(self._L.pn_export_diag_rhs(self.handle, ctypes.c_void_p(d.data_ptr()),
+            _lib.check(self._L.pn_export_diag_rhs(self.handle, None if d is None else ctypes.c_void_p(d.data_ptr()),
                                                   ctypes.c_void_p(r.data_ptr()), _stream(self._torch)))
         return d, r
 
@@ -464,13 +466,13 @@ def assemble(program, spec, device=0):
     if is_general(program):
         csr, q = assemble_general(program, spec, device=device)
         return SparseSystem(A=CsrOperator(csr), Q=q.cpu().numpy(), res=tuple(spec.res), n_unknowns=csr.U)
-    tables = as_tables(program)
+    tables = as_tables(program, dim=len(tuple(spec.res)))
     ctx = PnContext(tables, spec.res, spec.h, device=device)
     ctx.set_fields(spec)
     if bc == "neumann":
         csr, q = ctx.assemble_csr("neumann")
         return SparseSystem(A=CsrOperator(csr), Q=q.cpu().numpy(), res=tuple(spec.res), n_unknowns=tables.U)
-    Q = ctx.diag_rhs()[1].cpu().numpy()
+    Q = ctx.diag_rhs(diag=False)[1].cpu().numpy()
     return SparseSystem(A=StencilOperator(ctx), Q=Q, res=tuple(spec.res), n_unknowns=tables.U)
 
 
@@ -496,24 +498,30 @@ def solve_normal_cg(system, tol=1e-8, max_iter=50000, primal_tol=None, jacobi=Fa
 
 
 def unstagger(u, program, res, device=0):
-    """Collocated (*res, U) coefficients (solver.py:275-296) on the device."""
+    """Collocated (*res, U) coefficients (solver.py:275-296) on the device.
+    Context-free (pn_unstagger_grid): only the component parities are
+    uploaded; no operator context, no scratch vectors."""
     from .general import compile_general, is_general
+    torch = _torch()
     if is_general(program):
-        torch = _torch()
         gt = compile_general(program, 1.0)
-        res3 = _res3(res)
-        dev = torch.device("cuda", int(device))
-        ut = torch.as_tensor(np.asarray(u, np.float64), device=dev).contiguous()
-        out = torch.empty(res3 + (gt.U,), dtype=torch.float64, device=dev)
-        with torch.cuda.device(int(device)):
-            _lib.check(_lib.load().pn_unstagger_grid(gt.par.ctypes.data_as(ctypes.c_void_p), gt.U, *res3,
-                                                     ctypes.c_void_p(ut.data_ptr()), ctypes.c_void_p(out.data_ptr()),
-                                                     _stream(torch)))
-        out = out.cpu().numpy()
-        return out[:, :, 0] if len(tuple(res)) == 2 else out
-    tables = as_tables(program)
-    ctx = PnContext(tables, res, 1.0, device=device)
-    return ctx.unstagger(u).cpu().numpy()
+        par, U = gt.par, gt.U
+    else:
+        tables = as_tables(program, dim=len(tuple(res)))
+        par, U = np.ascontiguousarray(pack_tables(tables, 1.0)["par"], np.int32), tables.U
+    res3 = _res3(res)
+    dev = torch.device("cuda", int(device))
+    ut = u.to(dev, torch.float64).contiguous() if torch.is_tensor(u) else \
+        torch.from_numpy(np.ascontiguousarray(u, np.float64)).to(dev)
+    if ut.numel() != int(np.prod(res3)) * U:
+        raise ValueError(f"u has {ut.numel()} entries, expected {int(np.prod(res3)) * U}")
+    out = torch.empty(res3 + (U,), dtype=torch.float64, device=dev)
+    with torch.cuda.device(int(device)):
+        _lib.check(_lib.load().pn_unstagger_grid(par.ctypes.data_as(ctypes.c_void_p), U, *res3,
+                                                 ctypes.c_void_p(ut.data_ptr()), ctypes.c_void_p(out.data_ptr()),
+                                                 _stream(torch)))
+    out = out.cpu().numpy()
+    return out[:, :, 0] if len(tuple(res)) == 2 else out
 
 
 # ---------------------------------------------------------------------------
@@ -632,35 +640,60 @@ def reconstruct_radiance(collocated, unknowns, spec, x, omega, device=0):
 
 
 def solve_pn(program_or_N, spec, tol=1e-8, max_iter=50000, primal_tol=None, jacobi=False, x0=None,
-             mode="fast", device=0, return_staggered=False, **kw):
+             mode="fast", device=None, return_staggered=False, world=1, rank=0, nccl_id=None, out=None, **kw):
     """The north-star entry point: order + fields in, (N+1)^2 collocated SH
-    coefficients per voxel out (cli.py:136-155 without file I/O)."""
+    coefficients per voxel out (cli.py:136-155 without file I/O).
+
+    Multi-GPU (``world > 1``, one process per GPU): this rank solves the
+    z-slab ``distributed.slab_bounds(nz, world, rank)`` of the global system
+    with NCCL halo exchanges and rank-count-independent reductions, and
+    returns its planes of the collocated grid, shape (nx, ny, nz/world, U).
+    ``spec`` may hold the global fields or only this rank's planes
+    (``spec.z_planes``, configs.make_config(..., planes=)); ``nccl_id`` is
+    shared through torch.distributed when not given.  ``out``: optional host
+    array (e.g. pinned) the collocated result is copied into and returned."""
+    import os
     from .general import is_general
+    if tol <= 0:
+        raise ValueError("tolerance must be positive")
+    if device is None:   # one process per GPU: the local rank's device
+        device = int(os.environ.get("LOCAL_RANK", rank)) if world > 1 else 0
     if is_general(program_or_N):
+        if world > 1:
+            raise NotImplementedError("general (CDA) programs are single-GPU")
         _check_dim(program_or_N, spec)
-        if tol <= 0:
-            raise ValueError("tolerance must be positive")
         csr, q = assemble_general(program_or_N, spec, device=device)
         x, rep = csr.solve(tol=tol, max_iter=max_iter, primal_tol=primal_tol, jacobi=jacobi, x0=x0, b=q, mode=mode,
                            **kw)
-        coll = csr.unstagger(x).cpu().numpy()
-        if return_staggered:
-            return coll, rep, x.cpu().numpy()
-        return coll, rep
-    tables = as_tables(program_or_N)
+        return _finish(csr, x, rep, out, return_staggered)
+    tables = as_tables(program_or_N, dim=len(tuple(spec.res)))
     _check_dim(tables, spec)
     bc = _bc(spec)
-    ctx = PnContext(tables, spec.res, spec.h, device=device)
-    ctx.set_fields(spec)
-    if tol <= 0:
-        raise ValueError("tolerance must be positive")
+    if world > 1:
+        from .distributed import make_rank_context
+        if bc != "dirichlet" or mode != "fast":
+            raise NotImplementedError("slab decomposition: Dirichlet, fast mode (faithful mode is single-GPU)")
+        ctx = make_rank_context(tables, spec, rank, world, device=device, nccl_id=nccl_id)
+    else:
+        ctx = PnContext(tables, spec.res, spec.h, device=device)
+        ctx.set_fields(spec)
     if bc == "neumann":
         csr, q = ctx.assemble_csr("neumann")
         x, rep = csr.solve(tol=tol, max_iter=max_iter, primal_tol=primal_tol, jacobi=jacobi, x0=x0, b=q, mode=mode,
                            **kw)
+        return _finish(csr, x, rep, out, return_staggered)
+    x, rep = ctx.solve(tol=tol, max_iter=max_iter, primal_tol=primal_tol, jacobi=jacobi, x0=x0, mode=mode, **kw)
+    return _finish(ctx, x, rep, out, return_staggered)
+
+
+def _finish(ctx, x, rep, out, return_staggered):
+    dev_coll = ctx.unstagger(x)
+    if out is not None:
+        import torch
+        torch.from_numpy(out).view(dev_coll.shape).copy_(dev_coll)
+        coll = out
     else:
-        x, rep = ctx.solve(tol=tol, max_iter=max_iter, primal_tol=primal_tol, jacobi=jacobi, x0=x0, mode=mode, **kw)
-    coll = ctx.unstagger(x).cpu().numpy()
+        coll = dev_coll.cpu().numpy()
     if return_staggered:
         return coll, rep, x.cpu().numpy()
     return coll, rep

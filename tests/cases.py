@@ -30,7 +30,7 @@ CASES = [
 
 
 # 2-D programs (checkerboard, problems.py:104-127): (name, N, res); tables
-# come from tests/golden/tables_N{N}_2d.json, the spec from make_checkerboard
+# from the restated 2-D builder (build_tables(N, 2)), the spec from make_checkerboard
 CASES_2D = [
     ("cb_p1_15", 1, 15),
     ("cb_p2_15", 2, 15),
@@ -78,11 +78,9 @@ def cda_inputs(name):
 
 
 def tables_2d(N):
-    import json
-    import pathlib
-    from paper_1807_00410_b200.program import from_json
-    g = pathlib.Path(__file__).resolve().parent / "golden" / f"tables_N{N}_2d.json"
-    return from_json(json.loads(g.read_text()))
+    """Restated 2-D builder (equal to the reference fixtures, test_program.py)."""
+    from paper_1807_00410_b200.program import build_tables
+    return build_tables(N, dim=2)
 
 
 def rand_spec(N, res, seed, g=0.6, q_frac=0.5, uniform_sigma=False):

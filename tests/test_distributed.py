@@ -11,7 +11,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_1807_00410_b200.distributed import exchange_halos_cpu, plane_sum_reduce_cpu, slab_bounds
+from paper_1807_00410_b200.distributed import slab_bounds
+from slab_protocol import exchange_halos_cpu, plane_sum_reduce_cpu
 
 
 def _free_port():

@@ -89,6 +89,25 @@ def test_2d_tables_roundtrip_golden(N, golden):
     assert set(pk["par"].tolist()) <= {0, 1, 2, 3}     # no z staggering in 2-D
 
 
+@pytest.mark.parametrize("N", [1, 2, 3, 4, 5])
+def test_2d_builder_matches_reference_fixtures(N, golden):
+    """build_tables(N, 2) restates compile_program(build_pn(N, 2))
+    (equations.py:51-103,179-210): equal to the reference's tables."""
+    from paper_1807_00410_b200.program import build_tables
+    t = build_tables(N, dim=2)
+    assert t.dim == 2
+    assert to_json(t) == json.loads((golden["dir"] / f"tables_N{N}_2d.json").read_text())
+
+
+@pytest.mark.reference
+@pytest.mark.parametrize("N", [1, 2, 3, 4, 5, 6])
+def test_2d_builder_matches_live_reference(N, ref):
+    from pnrte.equations import build_pn
+    from pnrte.stencil import compile_program
+    from paper_1807_00410_b200.program import build_tables
+    assert to_json(build_tables(N, dim=2)) == to_json(tables_from_program(compile_program(build_pn(N, 2))))
+
+
 @pytest.mark.reference
 @pytest.mark.parametrize("N", [1, 2, 3])
 def test_2d_tables_match_live_reference(N, ref, golden):
