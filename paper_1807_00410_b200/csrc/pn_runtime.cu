@@ -1117,6 +1117,17 @@ int pn_bench(pn_context *c, int32_t what, int32_t reps, double *ms_per, void *st
         PN_TRY(to_solve_layout(c, seg, c->tmp.p, c->z.p, s));
         c->bench_ready = true;
     }
+    if (what == 6 || what == 7) {   // probe inputs: 6 = all-zero p and r, 7 = back to the dense fill
+        if (what == 6) {
+            PN_CUDA(cudaMemsetAsync(c->p.p, 0, c->R_s() * sizeof(double), s));
+            PN_CUDA(cudaMemsetAsync(c->r.p, 0, c->R_s() * sizeof(double), s));
+        }
+        c->bench_ready = what == 6;
+        *ms_per = 0.0;
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        return PN_OK;
+    }
     if (what == 1 || what == 3 || what == 4 || what == 5) {
         State h{};
         h.tol = 1e-300; h.primal_tol = -1; h.max_iter = 1LL << 40; h.rho = 1.0; h.norm_b = 1.0; h.norm_atb = 1.0;
