@@ -372,8 +372,13 @@ def slab_planes(nz, world, rank):
 
 def plane_digests(x, nzl):
     """sha256 of every local z-plane of a reference-layout slab vector."""
-    a = x.cpu().numpy().reshape(nzl, -1)
+    a = (x.cpu().numpy() if hasattr(x, "cpu") else np.asarray(x)).reshape(nzl, -1)
     return [hashlib.sha256(a[k].tobytes()).hexdigest() for k in range(nzl)]
+
+
+def global_digest(parts):
+    """sha256 over the plane digests of all ranks in rank (= global plane) order."""
+    return hashlib.sha256("".join(d for part in parts for d in part).encode()).hexdigest()
 
 
 def solve_checksum(D, ctx, nzl, iters=50):
@@ -381,8 +386,7 @@ def solve_checksum(D, ctx, nzl, iters=50):
     global plane order and over the residual history -- independent of the
     rank count when the solve is (slab reductions in plane order)."""
     x, rep = ctx.solve(tol=1e-300, max_iter=iters)
-    dig = [d for part in D.gather(plane_digests(x, nzl)) for d in part]
-    h = hashlib.sha256("".join(dig).encode()).hexdigest()
+    h = global_digest(D.gather(plane_digests(x, nzl)))
     hist = hashlib.sha256(np.asarray(rep.normal_history, np.float64).tobytes()).hexdigest()
     return {"iterations": rep.iterations, "x_plane_digest_sha256": h, "normal_history_sha256": hist,
             "normal_history_last": rep.normal_history[-1] if rep.normal_history else None,

@@ -96,3 +96,52 @@ def test_slab_bounds():
     assert slab_bounds(256, 8, 3) == (96, 32)
     with pytest.raises(ValueError):
         slab_bounds(10, 4, 0)
+
+
+def _digest_worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import bench
+        nz, plane = 12, 40
+        z0, nzl = slab_bounds(nz, world, rank)
+        x = np.random.default_rng(3).normal(size=nz * plane)
+        parts = [None] * world
+        dist.all_gather_object(parts, bench.plane_digests(x[z0 * plane:(z0 + nzl) * plane], nzl))
+        out[rank] = bench.global_digest(parts)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_solve_checksum_is_rank_count_independent(world):
+    """bench.py's solve_check: per-plane digests gathered in rank order give
+    the digest of the whole vector for any slab decomposition."""
+    import bench
+    nz, plane = 12, 40
+    x = np.random.default_rng(3).normal(size=nz * plane)
+    want = bench.global_digest([bench.plane_digests(x, nz)])
+    out = mp.Manager().dict()
+    mp.spawn(_digest_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    assert set(out.values()) == {want}
+
+
+@pytest.mark.parametrize("nz,world", [(256, 2), (256, 8), (512, 8), (512, 4)])
+def test_slab_planes_cover_each_rank(nz, world):
+    """bench.slab_planes: each rank generates its slab plus the +1 plane its
+    field upload reads (clamped at nz), and make_rank_context accepts it."""
+    import bench
+    for rank in range(world):
+        z0, nzl, (k0, k1) = bench.slab_planes(nz, world, rank)
+        assert (z0, nzl) == slab_bounds(nz, world, rank)
+        assert k0 == z0 and k1 == min(z0 + nzl + 1, nz)
+
+
+def test_rank_context_rejects_uncovered_planes():
+    from paper_1807_00410_b200.configs import make_config
+    from paper_1807_00410_b200.distributed import make_rank_context
+    from paper_1807_00410_b200.program import build_tables
+    spec = make_config(3, n=16, planes=(0, 8)).spec     # rank 1 of 2 needs planes 8..15
+    with pytest.raises(ValueError, match="do not cover"):
+        make_rank_context(build_tables(5), spec, rank=1, world=2)
