@@ -562,7 +562,7 @@ def run_ours(args):
     # ---- config 5 (P5 512^3, 200 fixed iterations): 8 GPUs (38.7 GB per vector)
     cfg5 = None
     if (world == 8 or args.cfg5) and not args.weak:
-        cfg5 = run_cfg5(D, peak)
+        cfg5 = run_cfg5(D, peak, args.cfg5_n)
 
     # ---- single-GPU context: other configs, time to residual, paper problems
     others = ttr = paper = None
@@ -620,16 +620,17 @@ def run_ours(args):
         D.dist.destroy_process_group()
 
 
-def run_cfg5(D, peak):
+def run_cfg5(D, peak, n=512):
     """Config 5: P5 512^3 (4.83e9 unknowns), each rank generating only its
-    planes; per-apply Gunk/s and the fixed 200-iteration CGNR."""
+    planes; per-apply Gunk/s and the fixed 200-iteration CGNR.  (n < 512:
+    the same code path on a smaller grid, for validation on fewer GPUs.)"""
     import torch
     from paper_1807_00410_b200.configs import make_config
     from paper_1807_00410_b200.distributed import make_rank_context, share_nccl_id
     from paper_1807_00410_b200.program import build_tables
-    z0, nzl, planes = slab_planes(512, D.world, D.rank)
+    z0, nzl, planes = slab_planes(n, D.world, D.rank)
     t0 = time.perf_counter()
-    cfg = make_config(5, planes=planes)
+    cfg = make_config(5, n=n, planes=planes)
     nccl_id = share_nccl_id(D.rank, D.world) if D.world > 1 else None
     ctx = make_rank_context(build_tables(cfg.N), cfg.spec, D.rank, D.world, device=D.local, nccl_id=nccl_id)
     t_setup = D.allmax(time.perf_counter() - t0)
@@ -644,7 +645,7 @@ def run_cfg5(D, peak):
     torch.cuda.synchronize()
     secs = D.allmax(time.perf_counter() - t0)
     bytes_apply = 8 * nx * ny * nzl * (2 * U + 2)
-    out = {"config": f"cfg5 P5 512^3 on {D.world} GPUs", "unknowns": R, "setup_s": t_setup,
+    out = {"config": f"cfg5 P5 {n}^3 on {D.world} GPUs", "unknowns": R, "setup_s": t_setup,
            "apply_ms": ms, "apply_gunk_s": R / (ms / 1e3) / 1e9,
            "roofline_per_gpu": {"achieved": bytes_apply / (ms / 1e3) / 1e9, "peak": peak,
                                 "frac": bytes_apply / (ms / 1e3) / 1e9 / peak, "unit": "GB/s"},
@@ -781,6 +782,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--weak", action="store_true", help="256x256x(256 N) P5 box, one 256^3 slab per GPU")
     ap.add_argument("--cfg5", action="store_true", help="config 5 at any N (needs >= 4 GPUs of memory)")
+    ap.add_argument("--cfg5-n", type=int, default=512, help="config-5 grid edge (validation runs on fewer GPUs)")
     ap.add_argument("--e2e-iters", type=int, default=50)
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--sustain-s", type=float, default=2.5)
