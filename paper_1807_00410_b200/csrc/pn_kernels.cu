@@ -12,6 +12,7 @@
 // This file is compiled with -fmad=false: faithful arithmetic must never be
 // contracted into FMAs (numpy / sparsetools do mul then add).  Kernels that
 // may use FMA live in pn_seg.cu.
+#include <atomic>
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <math.h>
@@ -601,7 +602,8 @@ int launch_dot(pn_context *c, const double *a, const double *b, int slot, cudaSt
 // accumulators over 32-blocks, fold hi+lo to 4x4 lanes, 4x4-lane FMA over
 // the 16-block remainder, lanewise ((a0+a1)+a2)+a3, (s0+s2)+(s1+s3), FMA
 // scalar tail.  Haswell kernel: 4x4-lane FMA over 16-blocks, fold to 2 lanes,
-// (h0+h1)+(h2+h3), lane sum, mul-then-add tail.  One warp per chunk.
+// (h0+h1)+(h2+h3), lane sum, mul-then-add tail.  One block per chunk; its
+// warp 0 carries the lane accumulators.
 __device__ __forceinline__ void chunk_range(long long n, int T, int t, long long &off, long long &width) {
     long long rem = n;
     off = 0;
@@ -613,10 +615,62 @@ __device__ __forceinline__ void chunk_range(long long n, int T, int t, long long
     }
 }
 
-__global__ void k_ddot_emul(const double *__restrict__ x, const double *__restrict__ y, long long n, int T, int kernel,
-                            double *out, const State *st) {
+// The lane accumulators are sequential FMA chains (that order IS the result), so
+// the speed comes from keeping the chain fed: all DD_THREADS threads of the
+// block stream the chunk through a DD_STAGES-deep cp.async ring of DD_TILE-element
+// tiles in shared memory, and warp 0 runs the chain over each landed tile
+// (one dependent DFMA per 32 / 16 elements, operands from shared memory).  A
+// one-warp version that loaded straight from HBM ran ~0.5 us per chain step:
+// 0.15 s per dot product at config 3 (75.5 M elements, 8 chunks).
+constexpr int DD_TILE = 2048, DD_STAGES = 5, DD_THREADS = 256;
+constexpr size_t DD_SMEM = (size_t)DD_STAGES * 2 * DD_TILE * sizeof(double);
+
+__device__ __forceinline__ void dd_cp8(double *dst_smem, const double *src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"((unsigned)__cvta_generic_to_shared(dst_smem)),
+                 "l"(src));
+}
+
+// acc = fma(x[i + lane], y[i + lane], acc) for i = 0, W, 2W, ... < nm (nm % W == 0), lanes < W of warp 0
+template <int W>
+__device__ __forceinline__ double dd_chain(const double *__restrict__ x, const double *__restrict__ y, long long nm,
+                                           double *sm) {
+    const int tid = threadIdx.x;
+    const long long ntiles = (nm + DD_TILE - 1) / DD_TILE;
+    auto issue = [&](long long t) {
+        if (t < ntiles) {
+            const long long base = t * DD_TILE;
+            const int cnt = (int)min((long long)DD_TILE, nm - base);
+            double *xs = sm + (size_t)(t % DD_STAGES) * 2 * DD_TILE, *ys = xs + DD_TILE;
+            for (int e = tid; e < cnt; e += DD_THREADS) {
+                dd_cp8(xs + e, x + base + e);
+                dd_cp8(ys + e, y + base + e);
+            }
+        }
+        asm volatile("cp.async.commit_group;\n" ::);
+    };
+    for (int t = 0; t < DD_STAGES - 1; ++t) issue(t);
+    double acc = 0.0;
+    for (long long t = 0; t < ntiles; ++t) {
+        issue(t + DD_STAGES - 1);   // refills the buffer consumed in iteration t - 1
+        asm volatile("cp.async.wait_group %0;\n" ::"n"(DD_STAGES - 1));
+        __syncthreads();
+        if (tid < W) {
+            const int cnt = (int)min((long long)DD_TILE, nm - t * DD_TILE);
+            const double *xs = sm + (size_t)(t % DD_STAGES) * 2 * DD_TILE + tid, *ys = xs + DD_TILE;
+#pragma unroll 8
+            for (int i = 0; i < cnt; i += W) acc = fma(xs[i], ys[i], acc);
+        }
+        __syncthreads();
+    }
+    return acc;
+}
+
+__global__ void __launch_bounds__(DD_THREADS) k_ddot_emul(const double *__restrict__ x, const double *__restrict__ y,
+                                                          long long n, int T, int kernel, double *out,
+                                                          const State *st) {
+    extern __shared__ __align__(16) double dd_sm[];
     if (st && stopped(st)) return;
-    const int lane = threadIdx.x;
+    const int lane = threadIdx.x & 31;
     long long off, w;
     if (n <= 10000 || T <= 1) { off = 0; w = n; }
     else chunk_range(n, T, blockIdx.x, off, w);
@@ -626,8 +680,9 @@ __global__ void k_ddot_emul(const double *__restrict__ x, const double *__restri
     if (kernel == 0) {
         const long long n32 = w & ~31LL, n16 = w & ~15LL;
         const int q = lane >> 3, l8 = lane & 7;
-        double a8 = 0.0;
-        for (long long i = 0; i < n32; i += 32) a8 = fma(x[i + 8 * q + l8], y[i + 8 * q + l8], a8);
+        // a8[q][l8] += x[i + 8 q + l8] * y[...] over the 32-blocks (8 q + l8 == lane)
+        const double a8 = dd_chain<32>(x, y, n32, dd_sm);
+        if (threadIdx.x >= 32) return;
         // fold to 4 lanes per accumulator: a4[q][l] = a8[q][l] + a8[q][l+4]
         double hi = __shfl_down_sync(0xffffffffu, a8, 4);
         double a4 = __dadd_rn(a8, hi);   // valid for l8 < 4
@@ -645,10 +700,9 @@ __global__ void k_ddot_emul(const double *__restrict__ x, const double *__restri
         }
     } else {
         const long long n16 = w & ~15LL;
-        const int q = (lane >> 2) & 3, l4 = lane & 3;
-        double a4 = 0.0;
-        if (lane < 16)
-            for (long long i = 0; i < n16; i += 16) a4 = fma(x[i + 4 * q + l4], y[i + 4 * q + l4], a4);
+        // a4[q][l4] over the 16-blocks (4 q + l4 == lane, lanes 0..15)
+        const double a4 = dd_chain<16>(x, y, n16, dd_sm);
+        if (threadIdx.x >= 32) return;
         double hi = __shfl_down_sync(0xffffffffu, a4, 2);
         double h = __dadd_rn(a4, hi);   // valid at l4 < 2
         double h1 = __shfl_sync(0xffffffffu, h, 4 + (lane & 1));
@@ -661,14 +715,21 @@ __global__ void k_ddot_emul(const double *__restrict__ x, const double *__restri
             for (long long i = n16; i < w; ++i) dot = __dadd_rn(dot, __dmul_rn(y[i], x[i]));
         }
     }
-    if (lane == 0) out[blockIdx.x] = dot;
+    if (threadIdx.x == 0) out[blockIdx.x] = dot;
 }
 
 int launch_ddot_emul(pn_context *c, const double *a, const double *b, long long n, int slot, int threads, int kernel,
                      cudaStream_t s, bool gated) {
     int nb = (n <= 10000 || threads <= 1) ? 1 : threads;
     if (nb > 64) { set_error("blas_threads > 64"); return PN_ERR_INVALID; }
-    k_ddot_emul<<<nb, 32, 0, s>>>(a, b, n, threads, kernel, c->ddot_chunks + slot * 64, gated ? c->state : nullptr);
+    static std::atomic<unsigned long long> cfg_mask{0};   // the attribute is per device
+    const unsigned long long bit = 1ULL << (c->device & 63);
+    if (!(cfg_mask.load() & bit)) {
+        PN_CUDA(cudaFuncSetAttribute(k_ddot_emul, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DD_SMEM));
+        cfg_mask.fetch_or(bit);
+    }
+    k_ddot_emul<<<nb, DD_THREADS, DD_SMEM, s>>>(a, b, n, threads, kernel, c->ddot_chunks + slot * 64,
+                                                gated ? c->state : nullptr);
     PN_CUDA(cudaGetLastError());
     c->launches++;
     return PN_OK;
