@@ -157,7 +157,7 @@ typedef struct {
     int32_t jacobi;
     int32_t mode;                /* 0 fast, 1 faithful */
     int32_t blas_threads;        /* faithful: OpenBLAS thread count to emulate */
-    int32_t blas_kernel;         /* faithful: 0 SkylakeX, 1 Haswell */
+    int32_t blas_kernel;         /* faithful: 0 SkylakeX, 1 Haswell; 2 = pairwise order (noise-floor probe, no OpenBLAS twin) */
     int32_t check_every;         /* host polls the device stop flag every k iterations (0 = auto) */
 } pn_solve_opts;
 

@@ -622,6 +622,8 @@ __device__ __forceinline__ void chunk_range(long long n, int T, int t, long long
 // (one dependent DFMA per 32 / 16 elements, operands from shared memory).  A
 // one-warp version that loaded straight from HBM ran ~0.5 us per chain step:
 // 0.15 s per dot product at config 3 (75.5 M elements, 8 chunks).
+__device__ __forceinline__ double tree256(double *sh);
+
 constexpr int DD_TILE = 2048, DD_STAGES = 5, DD_THREADS = 256;
 constexpr size_t DD_SMEM = (size_t)DD_STAGES * 2 * DD_TILE * sizeof(double);
 
@@ -698,6 +700,16 @@ __global__ void __launch_bounds__(DD_THREADS) k_ddot_emul(const double *__restri
             dot = n16 ? __dadd_rn(__dadd_rn(s0, s2), __dadd_rn(s1, s3)) : 0.0;
             for (long long i = n16; i < w; ++i) dot = fma(y[i], x[i], dot);
         }
+    } else if (kernel == 2) {
+        // not an OpenBLAS kernel: a pairwise-style order (thread-strided FMA partials,
+        // 256-leaf tree) for measuring the reference's own sensitivity to the dot
+        // order (SURVEY.md s8c protocol 3: "a different (pairwise) dot order")
+        __shared__ double sh[DD_THREADS];
+        double a = 0.0;
+        for (long long i = threadIdx.x; i < w; i += DD_THREADS) a = fma(x[i], y[i], a);
+        sh[threadIdx.x] = a;
+        __syncthreads();
+        dot = tree256(sh);
     } else {
         const long long n16 = w & ~15LL;
         // a4[q][l4] over the 16-blocks (4 q + l4 == lane, lanes 0..15)

@@ -483,6 +483,9 @@ __global__ void PN_SEG_BOUNDS(N) k_seg(
 #ifndef PN_RING_EXTRA
 #define PN_RING_EXTRA 8   // slots in flight beyond the consumers' (capped by shared memory)
 #endif
+#ifndef PN_RING_PF
+#define PN_RING_PF 148    // L2 prefetch distance in row groups ahead of the staged one; 0 disables
+#endif
 #ifndef PN_RING_YSM
 #define PN_RING_YSM 0     // 1: y neighbours inside a row group read from their ring slots
 #endif
@@ -603,6 +606,16 @@ __global__ void __launch_bounds__(RingTune<N>::threads, 1) k_seg_ring(
                 } else {         // ragged last row block: nothing to copy
                     if (lane == 0) mbar_arrive(full + slot);
                     cp_async_mbar_arrive(full + slot);
+                }
+                if constexpr (PN_RING_PF > 0) {
+                    // warm L2 with the row PN_RING_PF row groups ahead in the traversal: the
+                    // z + 1 neighbour rows (one plane of a y-tile ahead) are then L2 hits
+                    // instead of demand misses on the consumers' critical path
+                    if (lane == 0 && vb + PN_RING_PF < nvb) {
+                        const SegItem nx = seg_item<N>(g, vb + PN_RING_PF, rw);
+                        if (nx.j < g.ny)
+                            bulk_prefetch_l2(X + nx.rowbase, (unsigned)((N + 1) * (N + 1) * 32 * sizeof(double)));
+                    }
                 }
                 if (++slot == S) { slot = 0; ph ^= 1; }
             }
