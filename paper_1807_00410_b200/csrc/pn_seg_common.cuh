@@ -464,18 +464,11 @@ __global__ void PN_SEG_BOUNDS(N) k_seg(
 // between waiting for their rows and computing them, the copies of the next
 // rows are always in flight behind the arithmetic of the current ones.
 // Outputs, reduction partial slots and summation order are those of k_seg.
-#ifndef PN_RING_WG
-#define PN_RING_WG 0      // 1: producer in its own warpgroup, registers moved to the consumers (setmaxnreg)
-#endif
 #ifndef PN_RING_CONS
-#if PN_RING_WG
-#define PN_RING_CONS(N) ((N) >= 3 && (N) != 5 ? 6 : 12)
-#else
-#define PN_RING_CONS(N) ((N) >= 3 && (N) != 5 ? 7 : 14)
-#endif
+#define PN_RING_CONS(N) ((N) >= 3 && (N) != 5 ? 6 : 12)   // rows in compute (warp pairs or warps: whole warpgroups)
 #endif
 #ifndef PN_RING_REG_CONS
-#define PN_RING_REG_CONS 152
+#define PN_RING_REG_CONS 152   // registers per consumer thread after the producers hand theirs over
 #endif
 #ifndef PN_RING_REG_PROD
 #define PN_RING_REG_PROD 40
@@ -487,20 +480,23 @@ __global__ void PN_SEG_BOUNDS(N) k_seg(
 #define PN_RING_PF 148    // L2 prefetch distance in row groups ahead of the staged one; 0 disables
 #endif
 #ifndef PN_RING_YSM
-#define PN_RING_YSM 0     // 1: y neighbours inside a row group read from their ring slots
+#define PN_RING_YSM 1     // 1: y neighbours inside a row group read from their ring slots
 #endif
 constexpr size_t RING_SMEM_MAX = 232448;   // 227 KB opt-in per CTA
 constexpr size_t RING_HDR = 1024;          // full / empty mbarriers
+
+constexpr int RING_PROD = 4;   // producer warps: one warpgroup
 
 template <int N> struct RingTune {
     static constexpr int wpr = SegTune<N>::wpr;
     static constexpr int cons = PN_RING_CONS(N);
     static constexpr int fit = (int)((RING_SMEM_MAX - RING_HDR) / seg_smem_per_warp<N>());
     static constexpr int slots = fit < cons + PN_RING_EXTRA ? fit : cons + PN_RING_EXTRA;
-    static constexpr int threads = PN_RING_WG ? 32 * (cons * wpr + 4) : 32 * (cons * wpr + 1);
-    static_assert(!PN_RING_WG || (cons * wpr) % 4 == 0, "ring: consumers must fill whole warpgroups");
+    static constexpr int threads = 32 * (cons * wpr + RING_PROD);
+    static_assert((cons * wpr) % 4 == 0, "ring: consumers must fill whole warpgroups");
     static_assert(slots > cons, "ring: no slot left to stage ahead");
-    static_assert(slots * (2 * sizeof(unsigned long long) + sizeof(unsigned)) <= RING_HDR, "ring: header too small");
+    static_assert(slots > SegTune<N>::rows, "ring: a row group must fit the ring");
+    static_assert(slots * (2 * sizeof(unsigned long long) + sizeof(unsigned)) + 16 <= RING_HDR, "ring: header too small");
 };
 
 __device__ __forceinline__ void mbar_arrive_n(unsigned long long *b, int n) {
@@ -562,12 +558,13 @@ __global__ void __launch_bounds__(RingTune<N>::threads, 1) k_seg_ring(
     const double *__restrict__ ss, double *__restrict__ partials, long long slot_stride, int rb, const State *state) {
     extern __shared__ __align__(128) unsigned char ring_raw[];
     using T = RingTune<N>;
-    constexpr int WPR = T::wpr, S = T::slots, P = T::cons, ROWS = SegTune<N>::rows;
+    constexpr int WPR = T::wpr, S = T::slots, P = T::cons, ROWS = SegTune<N>::rows, Q = RING_PROD;
     constexpr bool YS = PN_RING_YSM != 0;   // y neighbours of the same row group from their ring slots
     constexpr int SW = (int)(seg_smem_per_warp<N>() / sizeof(double));
     constexpr unsigned END = 0xffffffffu;
     unsigned long long *full = reinterpret_cast<unsigned long long *>(ring_raw), *empty = full + S;
     volatile unsigned *meta = reinterpret_cast<volatile unsigned *>(empty + S);   // row group of the staged row
+    volatile unsigned *tkt = meta + S;                                            // ticket of group m at [m & 1]
     double *buf = reinterpret_cast<double *>(ring_raw + RING_HDR);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (threadIdx.x < S) {
@@ -576,30 +573,30 @@ __global__ void __launch_bounds__(RingTune<N>::threads, 1) k_seg_ring(
     }
     __syncthreads();
     if (state && seg_stopped(state)) return;    // CTA-uniform, before any copy or ticket
-#if PN_RING_WG
-    if (warp >= P * WPR) {
+    if (warp >= P * WPR) {   // ---- producers: one warpgroup, warp q stages rows q, q + Q, ... of every row group
         asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(PN_RING_REG_PROD));
-        if (warp != P * WPR) return;
-    } else {
-        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(PN_RING_REG_CONS));
-    }
-#endif
-    if (warp == P * WPR) {   // ---- producer
         // Row groups are handed out by a device-wide ticket in launch order, as the
         // hardware hands out the CTAs of k_seg: all SMs work inside one narrow
         // window of the traversal, so the z neighbour rows are L2 hits (a static
         // b, b + G, ... assignment lets the SMs drift apart: 2.5x the DRAM reads).
+        // One warp staged a row in ~1.5 us of dependent issue, twice what the SM
+        // needs; the four warps of the group stage four rows side by side.
+        const int q = warp - P * WPR;
         unsigned *tk = g.ticket;
-        int slot = 0, n = 0;
-        unsigned ph = 1;     // parity of the previous use's "empty" completion (first pass: no wait)
-        unsigned next = lane == 0 ? atomicAdd(tk, 1u) : 0u;
-        for (;;) {
-            const unsigned vb = __shfl_sync(0xffffffffu, next, 0);
+        unsigned next = (q == 0 && lane == 0) ? atomicAdd(tk, 1u) : 0u;
+        int m = 0;
+        for (;; ++m) {
+            if (q == 0 && lane == 0) {
+                tkt[m & 1] = next;
+                if (next < nvb) next = atomicAdd(tk, 1u);   // in flight behind this group's staging
+            }
+            asm volatile("bar.sync 1, %0;\n" ::"n"(32 * Q) : "memory");
+            const unsigned vb = tkt[m & 1];
             if (vb >= nvb) break;
-            if (lane == 0) next = atomicAdd(tk, 1u);   // in flight behind this group's staging
-            for (int rw = 0; rw < ROWS; ++rw, ++n) {
+            for (int rw = q; rw < ROWS; rw += Q) {
+                const int n = m * ROWS + rw, use = n / S, slot = n - use * S;
                 const SegItem it = seg_item<N>(g, vb, rw);
-                if (n >= S) mbar_wait(empty + slot, ph);
+                if (use > 0) mbar_wait(empty + slot, (unsigned)(use - 1) & 1u);
                 if (lane == 0) meta[slot] = vb;
                 if (it.j < g.ny) {
                     ring_stage<N>(g, it, buf + (size_t)slot * SW, X, st, ss, lane, full + slot);
@@ -608,29 +605,26 @@ __global__ void __launch_bounds__(RingTune<N>::threads, 1) k_seg_ring(
                     cp_async_mbar_arrive(full + slot);
                 }
                 if constexpr (PN_RING_PF > 0) {
-                    // warm L2 with the row PN_RING_PF row groups ahead in the traversal: the
-                    // z + 1 neighbour rows (one plane of a y-tile ahead) are then L2 hits
-                    // instead of demand misses on the consumers' critical path
+                    // warm L2 with the row PN_RING_PF row groups ahead in the traversal
                     if (lane == 0 && vb + PN_RING_PF < nvb) {
                         const SegItem nx = seg_item<N>(g, vb + PN_RING_PF, rw);
                         if (nx.j < g.ny)
                             bulk_prefetch_l2(X + nx.rowbase, (unsigned)((N + 1) * (N + 1) * 32 * sizeof(double)));
                     }
                 }
-                if (++slot == S) { slot = 0; ph ^= 1; }
             }
         }
-        for (int q = 0; q < P; ++q, ++n) {   // one end marker per consumer
-            if (n >= S) mbar_wait(empty + slot, ph);
+        for (int e = q; e < P; e += Q) {   // one end marker per consumer
+            const int n = m * ROWS + e, use = n / S, slot = n - use * S;
+            if (use > 0) mbar_wait(empty + slot, (unsigned)(use - 1) & 1u);
             if (lane == 0) {
                 meta[slot] = END;
                 mbar_arrive(full + slot);
             }
             cp_async_mbar_arrive(full + slot);
-            if (++slot == S) { slot = 0; ph ^= 1; }
         }
         // every CTA drew exactly one ticket >= nvb; the last one to get here rewinds the counters
-        if (lane == 0) {
+        if (q == 0 && lane == 0) {
             __threadfence();
             if (atomicAdd(tk + 1, 1u) == gridDim.x - 1) {
                 tk[0] = 0;
@@ -639,6 +633,7 @@ __global__ void __launch_bounds__(RingTune<N>::threads, 1) k_seg_ring(
         }
         return;
     }
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(PN_RING_REG_CONS));
     // ---- consumers: row pair (or warp) p takes the staged rows p, p + P, ...
     const int p = warp / WPR, half = warp % WPR;
     int slot = p;

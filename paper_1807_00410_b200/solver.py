@@ -59,6 +59,18 @@ class SolveReport:
     primal_history: list = field(default_factory=list)
 
 
+@dataclass
+class SolutionField:
+    """Mirror of the reference's result record (solver.py:53-59): the staggered
+    solution, the collocated (*res, U) grid, the (l, m) of each component, the
+    solved spec and the report.  ``solve_pn(..., as_field=True)`` returns one."""
+    staggered: object
+    collocated: object
+    unknowns: list
+    spec: object
+    report: SolveReport
+
+
 def _torch():
     import torch
     if not torch.cuda.is_available():
@@ -640,7 +652,8 @@ def reconstruct_radiance(collocated, unknowns, spec, x, omega, device=0):
 
 
 def solve_pn(program_or_N, spec, tol=1e-8, max_iter=50000, primal_tol=None, jacobi=False, x0=None,
-             mode="fast", device=None, return_staggered=False, world=1, rank=0, nccl_id=None, out=None, **kw):
+             mode="fast", device=None, return_staggered=False, world=1, rank=0, nccl_id=None, out=None,
+             as_field=False, **kw):
     """The north-star entry point: order + fields in, (N+1)^2 collocated SH
     coefficients per voxel out (cli.py:136-155 without file I/O).
 
@@ -651,7 +664,14 @@ def solve_pn(program_or_N, spec, tol=1e-8, max_iter=50000, primal_tol=None, jaco
     ``spec`` may hold the global fields or only this rank's planes
     (``spec.z_planes``, configs.make_config(..., planes=)); ``nccl_id`` is
     shared through torch.distributed when not given.  ``out``: optional host
-    array (e.g. pinned) the collocated result is copied into and returned."""
+    array (e.g. pinned) the collocated result is copied into and returned.
+    ``as_field``: return a ``SolutionField`` (the reference's record,
+    solver.py:53-59) instead of the (collocated, report) pair."""
+    if as_field:
+        coll, rep, stag = solve_pn(program_or_N, spec, tol, max_iter, primal_tol, jacobi, x0, mode, device, True,
+                                   world, rank, nccl_id, out, False, **kw)
+        prog = program_or_N if not isinstance(program_or_N, int) else as_tables(program_or_N, dim=len(tuple(spec.res)))
+        return SolutionField(stag, coll, unknown_order(prog), spec, rep)
     import os
     from .general import is_general
     if tol <= 0:

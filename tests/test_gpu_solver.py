@@ -140,6 +140,12 @@ def test_solve_pn_end_to_end():
     assert rep.converged and coll.shape == (32, 32, 32, 36)
     o = StencilOracle(build_tables(cfg.N), spec)
     assert coll.tobytes() == o.unstagger(xs).tobytes()
+    # the reference's result record (solver.py:53-59) through the package-level names
+    import paper_1807_00410_b200 as pkg
+    f = pkg.solve_pn(cfg.N, spec, tol=1e-6, max_iter=20000, as_field=True)
+    assert isinstance(f, pkg.SolutionField) and f.spec is spec and f.report.iterations == rep.iterations
+    assert f.collocated.tobytes() == coll.tobytes() and f.staggered.tobytes() == xs.tobytes()
+    assert f.unknowns[:4] == [(0, 0), (1, -1), (1, 0), (1, 1)] and len(f.unknowns) == 36
 
 
 def _group(tables, spec, n_slabs):
