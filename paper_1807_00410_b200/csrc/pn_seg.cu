@@ -14,16 +14,12 @@
 
 namespace pn {
 
-constexpr unsigned RING_TICKETS = 16;
-
 struct SegCtx {
     SegParams *pa = nullptr, *pt = nullptr;   // host parameter blocks (A, A^T)
     SegGeo g{};
     bool ok = false;
     double *sig_pad = nullptr;                // padded sigma_t / sigma_s slabs (nx % 32 != 0)
     size_t sig_pad_n = 0;                     // doubles per field
-    unsigned *tickets = nullptr;              // ring path: RING_TICKETS {next, finished} pairs, zero between launches
-    unsigned tick_i = 0;
 };
 
 static bool seg_padded(const pn_context *c) { return c->g.nx % 32 != 0; }
@@ -146,12 +142,6 @@ int pn_seg_prepare(pn_context *c, cudaStream_t s) {
     const double vec_mb = (double)c->g.nzl * c->g.plane * sizeof(double) / 1e6;
     g.bulk = vec_mb > 96.0;
     if (const char *e = getenv("PNRTE_SEG_BULK")) g.bulk = atoi(e) != 0;
-    g.ring = 0;
-    if (const char *e = getenv("PNRTE_SEG_RING")) g.ring = atoi(e) != 0;
-    if (g.ring && !sc->tickets) {
-        PN_CUDA(cudaMalloc(&sc->tickets, 2 * RING_TICKETS * sizeof(unsigned)));
-        PN_CUDA(cudaMemsetAsync(sc->tickets, 0, 2 * RING_TICKETS * sizeof(unsigned), s));
-    }
     sc->ok = true;
     return PN_OK;
 }
@@ -164,9 +154,6 @@ int pn_seg_apply(pn_context *c, int trans, const double *x, double *y, int red, 
     g.kst = kst;
     g.npl = npl < 0 ? c->g.nzl : npl;
     if (g.npl <= 0) return PN_OK;
-    // consecutive launches (which may overlap: interior and boundary planes on
-    // two streams) draw their row groups from different ticket pairs
-    g.ticket = g.ring ? sc->tickets + 2 * (sc->tick_i++ % RING_TICKETS) : nullptr;
     const SegParams &prm = trans ? *sc->pt : *sc->pa;
     const long long stride = (long long)c->g.nz * c->red_bx;
     const State *st = gated ? c->state : nullptr;
@@ -246,7 +233,6 @@ void pn_seg_release(pn_context *c) {
     delete sc->pa;
     delete sc->pt;
     if (sc->sig_pad) cudaFree(sc->sig_pad);
-    if (sc->tickets) cudaFree(sc->tickets);
     delete sc;
     c->seg = nullptr;
 }

@@ -318,8 +318,8 @@ __device__ __forceinline__ void seg_pair_sync(int rw) {
 // compute one staged row: outputs (and fused reduction terms) of this warp's classes
 template <int N, int TRANS, int RED, bool JAC, bool TMA, bool PAD>
 __device__ __forceinline__ void seg_compute(const SegParams &prm, const SegGeo &g, const SegItem &it,
-                                            const double *xs, const double *ys_m, const double *ys_p,
-                                            const double *__restrict__ X, double *__restrict__ Y,
+                                            const double *xs, const double *__restrict__ X, double *__restrict__ Y,
+                                            int rw,
                                             const double *__restrict__ minv, double *__restrict__ zt, int lane,
                                             int half, RedAcc &ra) {
     constexpr int U = (N + 1) * (N + 1);
@@ -335,9 +335,10 @@ __device__ __forceinline__ void seg_compute(const SegParams &prm, const SegGeo &
     const double *Xl = X + it.rowbase + lane;
     r.Xym = it.j > 0 ? Xl - g.nseg * rowlen : nullptr;
     r.Xyp = it.j < g.ny - 1 ? Xl + g.nseg * rowlen : nullptr;
-    if constexpr (TMA) {   // y neighbours staged in this CTA's shared memory (ys_m / ys_p, null: global)
-        if (ys_m) r.Xym = ys_m + lane;
-        if (ys_p && r.Xyp) r.Xyp = ys_p + lane;
+    if constexpr (TMA) {   // y neighbours inside the CTA: the adjacent staged rows
+        constexpr int SW = (int)(seg_smem_per_warp<N>() / sizeof(double));
+        if (rw > 0) r.Xym = xs - SW + lane;
+        if (rw < SegTune<N>::rows - 1 && r.Xyp) r.Xyp = xs + SW + lane;
     }
     r.Xzm = it.kg > 0 ? Xl - g.plane : nullptr;
     r.Xzp = it.kg < g.nz - 1 ? Xl + g.plane : nullptr;
@@ -446,236 +447,9 @@ __global__ void PN_SEG_BOUNDS(N) k_seg(
             if (rw > 0) mbar_wait(seg_bar<N>(xs - SW), 0);
             if (rw < SegTune<N>::rows - 1 && it.j + 1 < g.ny) mbar_wait(seg_bar<N>(xs + SW), 0);
         }
-        seg_compute<N, TRANS, RED, JAC, TMA, PAD>(prm, g, it, xs, rw > 0 ? xs - SW : nullptr,
-                                                  rw < SegTune<N>::rows - 1 ? xs + SW : nullptr, X, Y, minv, zt, lane,
-                                                  half, ra);
+        seg_compute<N, TRANS, RED, JAC, TMA, PAD>(prm, g, it, xs, X, Y, rw, minv, zt, lane, half, ra);
     }
     seg_partial<N, RED, JAC>(g, it, ra, lane, warp, partials, slot_stride, rb);
-}
-
-// ---------------------------------------------------------------------------
-// Ring path ("persistent" apply for HBM-sized slabs): one CTA per SM walks the
-// same row-group sequence as the k_seg grid (virtual block b, b + G, ...).  A
-// producer warp keeps a ring of staged rows full — the own row by one
-// cp.async.bulk, sigma rows and segment-edge values by cp.async, all
-// completing on the slot's "full" mbarrier — while the consumer warps (one
-// warp, or a warp pair, per row) compute rows as they arrive and hand the slot
-// back through its "empty" mbarrier.  Unlike k_seg, whose CTAs alternate
-// between waiting for their rows and computing them, the copies of the next
-// rows are always in flight behind the arithmetic of the current ones.
-// Outputs, reduction partial slots and summation order are those of k_seg.
-#ifndef PN_RING_CONS
-#define PN_RING_CONS(N) ((N) >= 3 && (N) != 5 ? 6 : 12)   // rows in compute (warp pairs or warps: whole warpgroups)
-#endif
-#ifndef PN_RING_REG_CONS
-#define PN_RING_REG_CONS 152   // registers per consumer thread after the producers hand theirs over
-#endif
-#ifndef PN_RING_REG_PROD
-#define PN_RING_REG_PROD 40
-#endif
-#ifndef PN_RING_EXTRA
-#define PN_RING_EXTRA 8   // slots in flight beyond the consumers' (capped by shared memory)
-#endif
-#ifndef PN_RING_PF
-#define PN_RING_PF 148    // L2 prefetch distance in row groups ahead of the staged one; 0 disables
-#endif
-#ifndef PN_RING_YSM
-#define PN_RING_YSM 1     // 1: y neighbours inside a row group read from their ring slots
-#endif
-constexpr size_t RING_SMEM_MAX = 232448;   // 227 KB opt-in per CTA
-constexpr size_t RING_HDR = 1024;          // full / empty mbarriers
-
-constexpr int RING_PROD = 4;   // producer warps: one warpgroup
-
-template <int N> struct RingTune {
-    static constexpr int wpr = SegTune<N>::wpr;
-    static constexpr int cons = PN_RING_CONS(N);
-    static constexpr int fit = (int)((RING_SMEM_MAX - RING_HDR) / seg_smem_per_warp<N>());
-    static constexpr int slots = fit < cons + PN_RING_EXTRA ? fit : cons + PN_RING_EXTRA;
-    static constexpr int threads = 32 * (cons * wpr + RING_PROD);
-    static_assert((cons * wpr) % 4 == 0, "ring: consumers must fill whole warpgroups");
-    static_assert(slots > cons, "ring: no slot left to stage ahead");
-    static_assert(slots > SegTune<N>::rows, "ring: a row group must fit the ring");
-    static_assert(slots * (2 * sizeof(unsigned long long) + sizeof(unsigned)) + 16 <= RING_HDR, "ring: header too small");
-};
-
-__device__ __forceinline__ void mbar_arrive_n(unsigned long long *b, int n) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(b)), "r"(n) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(unsigned long long *b) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(b)) : "memory");
-}
-// arrive on b once all cp.async issued so far by this thread have landed (counted in the barrier's init count)
-__device__ __forceinline__ void cp_async_mbar_arrive(unsigned long long *b) {
-    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(b)) : "memory");
-}
-// 8-byte cp.async that zero-fills when !valid (src-size 0: nothing is read)
-__device__ __forceinline__ void cp_async8_z(void *dst_smem, const void *src, bool valid) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(dst_smem)), "l"(src),
-                 "r"(valid ? 8 : 0));
-}
-
-// producer warp: all copies of one row into slot buffer xs, completing on bar
-template <int N>
-__device__ __forceinline__ void ring_stage(const SegGeo &g, const SegItem &it, double *xs, const double *__restrict__ X,
-                                           const double *__restrict__ st, const double *__restrict__ ss, int lane,
-                                           unsigned long long *bar) {
-    constexpr int U = (N + 1) * (N + 1);
-    constexpr long long rowlen = (long long)U * 32;
-    double *ep = xs + 32 * U, *en = ep + U, *sg = en + U;
-    const double *Xrow = X + it.rowbase;
-    const bool has_prev = it.seg > 0, has_next = it.seg < g.nseg - 1;
-    if (lane == 0) {
-        mbar_expect_tx(bar, (unsigned)(rowlen * sizeof(double)));
-        bulk_g2s(xs, Xrow, (unsigned)(rowlen * sizeof(double)), bar);
-    }
-#pragma unroll
-    for (int q = lane; q < 128; q += 32) {
-        const int rowq = q >> 4, part = (q & 15) * 2, fld = rowq >> 2, r4 = rowq & 3;
-        const int jj = min(it.j + (r4 & 1), g.ny - 1);
-        const int kk = it.kl + (r4 >> 1);   // plane nzl exists (edge-replicated at upload)
-        const long long vb = ((long long)kk * g.ny + jj) * g.sx + it.seg * 32;
-        cp_async16(sg + fld * 136 + r4 * 34 + part, (fld ? ss : st) + vb + part);
-    }
-    if (lane < 8) {   // x+1 sample of lane 31 per sigma row, edge-replicated at nx-1
-        const int fld = lane >> 2, r4 = lane & 3;
-        const int jj = min(it.j + (r4 & 1), g.ny - 1);
-        const int kk = it.kl + (r4 >> 1);
-        const long long vb = ((long long)kk * g.ny + jj) * g.sx + it.seg * 32 + (has_next ? 32 : 31);
-        cp_async8(sg + fld * 136 + r4 * 34 + 32, (fld ? ss : st) + vb);
-    }
-    for (int c = lane; c < U; c += 32) {
-        cp_async8_z(ep + c, has_prev ? Xrow - rowlen + c * 32 + 31 : Xrow, has_prev);
-        cp_async8_z(en + c, has_next ? Xrow + rowlen + c * 32 : Xrow, has_next);
-    }
-    cp_async_mbar_arrive(bar);
-}
-
-template <int N, int TRANS, int RED, bool JAC, bool PAD>
-__global__ void __launch_bounds__(RingTune<N>::threads, 1) k_seg_ring(
-    const __grid_constant__ SegParams prm, SegGeo g, unsigned nvb, const double *__restrict__ X, double *__restrict__ Y,
-    const double *__restrict__ minv, double *__restrict__ zt, const double *__restrict__ st,
-    const double *__restrict__ ss, double *__restrict__ partials, long long slot_stride, int rb, const State *state) {
-    extern __shared__ __align__(128) unsigned char ring_raw[];
-    using T = RingTune<N>;
-    constexpr int WPR = T::wpr, S = T::slots, P = T::cons, ROWS = SegTune<N>::rows, Q = RING_PROD;
-    constexpr bool YS = PN_RING_YSM != 0;   // y neighbours of the same row group from their ring slots
-    constexpr int SW = (int)(seg_smem_per_warp<N>() / sizeof(double));
-    constexpr unsigned END = 0xffffffffu;
-    unsigned long long *full = reinterpret_cast<unsigned long long *>(ring_raw), *empty = full + S;
-    volatile unsigned *meta = reinterpret_cast<volatile unsigned *>(empty + S);   // row group of the staged row
-    volatile unsigned *tkt = meta + S;                                            // ticket of group m at [m & 1]
-    double *buf = reinterpret_cast<double *>(ring_raw + RING_HDR);
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (threadIdx.x < S) {
-        mbar_init(full + threadIdx.x, 33);      // expect_tx arrive of lane 0 + 32 cp.async completions
-        mbar_init(empty + threadIdx.x, (YS ? 3 : 1) * WPR);   // elected lanes of the warps that read the slot
-    }
-    __syncthreads();
-    if (state && seg_stopped(state)) return;    // CTA-uniform, before any copy or ticket
-    if (warp >= P * WPR) {   // ---- producers: one warpgroup, warp q stages rows q, q + Q, ... of every row group
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(PN_RING_REG_PROD));
-        // Row groups are handed out by a device-wide ticket in launch order, as the
-        // hardware hands out the CTAs of k_seg: all SMs work inside one narrow
-        // window of the traversal, so the z neighbour rows are L2 hits (a static
-        // b, b + G, ... assignment lets the SMs drift apart: 2.5x the DRAM reads).
-        // One warp staged a row in ~1.5 us of dependent issue, twice what the SM
-        // needs; the four warps of the group stage four rows side by side.
-        const int q = warp - P * WPR;
-        unsigned *tk = g.ticket;
-        unsigned next = (q == 0 && lane == 0) ? atomicAdd(tk, 1u) : 0u;
-        int m = 0;
-        for (;; ++m) {
-            if (q == 0 && lane == 0) {
-                tkt[m & 1] = next;
-                if (next < nvb) next = atomicAdd(tk, 1u);   // in flight behind this group's staging
-            }
-            asm volatile("bar.sync 1, %0;\n" ::"n"(32 * Q) : "memory");
-            const unsigned vb = tkt[m & 1];
-            if (vb >= nvb) break;
-            for (int rw = q; rw < ROWS; rw += Q) {
-                const int n = m * ROWS + rw, use = n / S, slot = n - use * S;
-                const SegItem it = seg_item<N>(g, vb, rw);
-                if (use > 0) mbar_wait(empty + slot, (unsigned)(use - 1) & 1u);
-                if (lane == 0) meta[slot] = vb;
-                if (it.j < g.ny) {
-                    ring_stage<N>(g, it, buf + (size_t)slot * SW, X, st, ss, lane, full + slot);
-                } else {         // ragged last row block: nothing to copy
-                    if (lane == 0) mbar_arrive(full + slot);
-                    cp_async_mbar_arrive(full + slot);
-                }
-                if constexpr (PN_RING_PF > 0) {
-                    // warm L2 with the row PN_RING_PF row groups ahead in the traversal
-                    if (lane == 0 && vb + PN_RING_PF < nvb) {
-                        const SegItem nx = seg_item<N>(g, vb + PN_RING_PF, rw);
-                        if (nx.j < g.ny)
-                            bulk_prefetch_l2(X + nx.rowbase, (unsigned)((N + 1) * (N + 1) * 32 * sizeof(double)));
-                    }
-                }
-            }
-        }
-        for (int e = q; e < P; e += Q) {   // one end marker per consumer
-            const int n = m * ROWS + e, use = n / S, slot = n - use * S;
-            if (use > 0) mbar_wait(empty + slot, (unsigned)(use - 1) & 1u);
-            if (lane == 0) {
-                meta[slot] = END;
-                mbar_arrive(full + slot);
-            }
-            cp_async_mbar_arrive(full + slot);
-        }
-        // every CTA drew exactly one ticket >= nvb; the last one to get here rewinds the counters
-        if (q == 0 && lane == 0) {
-            __threadfence();
-            if (atomicAdd(tk + 1, 1u) == gridDim.x - 1) {
-                tk[0] = 0;
-                tk[1] = 0;
-            }
-        }
-        return;
-    }
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(PN_RING_REG_CONS));
-    // ---- consumers: row pair (or warp) p takes the staged rows p, p + P, ...
-    const int p = warp / WPR, half = warp % WPR;
-    int slot = p;
-    unsigned ph = 0;
-    for (int n = p;; n += P) {
-        mbar_wait(full + slot, ph);
-        const unsigned vb = meta[slot];
-        if (vb == END) break;
-        const int rw = n % ROWS;
-        const SegItem it = seg_item<N>(g, vb, rw);
-        RedAcc ra;
-        if constexpr (YS) {
-            // rows n - 1 / n + 1 of the same row group are the y neighbours; a slot is
-            // handed back after its own row and both neighbours have read it (the
-            // group's end rows arrive for the neighbour they do not have)
-            const int sm = slot == 0 ? S - 1 : slot - 1, sp = slot + 1 == S ? 0 : slot + 1;
-            const unsigned pm = slot == 0 ? ph ^ 1 : ph, pp = slot + 1 == S ? ph ^ 1 : ph;
-            const bool hm = rw > 0, hp = rw < ROWS - 1;
-            if (hm) mbar_wait(full + sm, pm);
-            if (hp) mbar_wait(full + sp, pp);
-            if (it.j < g.ny)
-                seg_compute<N, TRANS, RED, JAC, true, PAD>(prm, g, it, buf + (size_t)slot * SW,
-                                                          hm ? buf + (size_t)sm * SW : nullptr,
-                                                          hp ? buf + (size_t)sp * SW : nullptr, X, Y, minv, zt, lane,
-                                                          half, ra);
-            __syncwarp();
-            if (lane == 0) {
-                mbar_arrive_n(empty + slot, 1 + (hm ? 0 : 1) + (hp ? 0 : 1));
-                if (hm) mbar_arrive(empty + sm);
-                if (hp) mbar_arrive(empty + sp);
-            }
-        } else {
-            if (it.j < g.ny)
-                seg_compute<N, TRANS, RED, JAC, false, PAD>(prm, g, it, buf + (size_t)slot * SW, nullptr, nullptr, X, Y,
-                                                           minv, zt, lane, half, ra);
-            __syncwarp();
-            if (lane == 0) mbar_arrive(empty + slot);
-        }
-        seg_partial<N, RED, JAC>(g, it, ra, lane, rw * WPR + half, partials, slot_stride, rb);
-        slot += P;
-        if (slot >= S) { slot -= S; ph ^= 1; }
-    }
 }
 
 template <int N>
@@ -695,46 +469,6 @@ int seg_launch(const SegParams &prm, const SegGeo &g0, int trans, int red, bool 
     if (g.nyb != (g.ny + rows - 1) / rows) { set_error("segmented launch: row blocking mismatch"); return PN_ERR_INVALID; }
     int dev = 0;
     PN_CUDA(cudaGetDevice(&dev));
-    if (g.ring) {   // persistent ring path: one CTA per SM
-        static std::atomic<int> sm_count[64];
-        int nsm = sm_count[dev & 63].load();
-        if (!nsm) {
-            PN_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-            sm_count[dev & 63].store(nsm);
-        }
-        const size_t rsmem = RING_HDR + (size_t)RingTune<N>::slots * seg_smem_per_warp<N>();
-        dim3 rgrid((unsigned)std::min<long long>(nblk, nsm)), rblock(RingTune<N>::threads);
-#define PN_RING_GO2(T, R, J, P)                                                                                   \
-    do {                                                                                                          \
-        static std::atomic<unsigned long long> cfg_mask{0};                                                       \
-        const unsigned long long bit_ = 1ULL << (dev & 63);                                                       \
-        if (!(cfg_mask.load() & bit_)) {                                                                          \
-            PN_CUDA(cudaFuncSetAttribute(k_seg_ring<N, T, R, J, P>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
-                                         (int)rsmem));                                                            \
-            cfg_mask.fetch_or(bit_);                                                                              \
-        }                                                                                                         \
-        k_seg_ring<N, T, R, J, P><<<rgrid, rblock, rsmem, s>>>(prm, g, (unsigned)nblk, x, y, minv, zt, st, ss,    \
-                                                               partials, slot_stride, rb, state);                 \
-    } while (0)
-#define PN_RING_GO(T, R, J)                          \
-    do {                                             \
-        if (g.sx != g.nx) PN_RING_GO2(T, R, J, true); \
-        else PN_RING_GO2(T, R, J, false);            \
-    } while (0)
-        if (!trans) {
-            if (red == 1) PN_RING_GO(0, 1, false);
-            else PN_RING_GO(0, 0, false);
-        } else if (red == 2) {
-            if (jac) PN_RING_GO(1, 2, true);
-            else PN_RING_GO(1, 2, false);
-        } else {
-            PN_RING_GO(1, 0, false);
-        }
-#undef PN_RING_GO
-#undef PN_RING_GO2
-        PN_CUDA(cudaGetLastError());
-        return PN_OK;
-    }
 #define PN_SEG_GO3(T, R, J, B, P)                                                                                 \
     do {                                                                                                          \
         /* the attribute is per device: one bit per device ordinal */                                           \

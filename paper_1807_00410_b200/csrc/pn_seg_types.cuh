@@ -51,8 +51,6 @@ struct SegGeo {
     int kl0, npl, kst;       // local planes kl0 + i*kst, i < npl, computed by one launch
     int sx;                  // row stride of the sigma slabs the kernel reads (nx, or nseg*32 when padded)
     int bulk;                // 1: bulk (TMA) staging path, for slabs far larger than L2
-    int ring;                // 1: persistent producer / consumer ring (k_seg_ring) instead of the k_seg grid
-    unsigned *ticket;        // ring: {next row group, CTAs finished} of this launch (zero between launches)
     long long plane, pvox;
     FastDiv dseg, dtyb, dnpl;   // set per launch by seg_launch (nseg, min(tyb, nyb), npl)
 };
