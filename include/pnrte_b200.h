@@ -212,6 +212,11 @@ int64_t pn_kernel_launches(pn_context *ctx);
 /* NCCL unique id (128 bytes) for multi-GPU creation (rank 0 calls it). */
 int pn_nccl_unique_id(void *out128);
 
+/* One-rank check of the NCCL call patterns of the slab path on `device`
+ * (communicator, grouped send/recv, in-place all-gather, captured into a CUDA
+ * graph on a forked stream and replayed) over n doubles; PN_OK or an error. */
+int pn_nccl_selftest(int device, int n);
+
 /* Loopback slab group: several contexts on ONE device whose halos and
  * partial sums are exchanged by device copies instead of NCCL (tests of the
  * slab decomposition on one GPU).  Contexts must be created with world > 1,

@@ -99,6 +99,7 @@ def load():
         "pn_unstagger": [P, P, P, P],
         "pn_solve_host": [P, ctypes.POINTER(SolveOpts), P, ctypes.POINTER(Report), P, P, I64],
         "pn_nccl_unique_id": [P],
+        "pn_nccl_selftest": [I32, I32],
         "pn_group_solve": [P, I32, ctypes.POINTER(SolveOpts), P, ctypes.POINTER(Report), P, P, I64, P],
         "pn_group_apply": [P, I32, I32, I32, P, P, P],
         "pn_bench": [P, I32, I32, ctypes.POINTER(F64), P],

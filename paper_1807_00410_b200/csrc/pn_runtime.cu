@@ -198,6 +198,78 @@ int pn_nccl_unique_id(void *out128) {
     return PN_OK;
 }
 
+// One-rank exercise of every NCCL call pattern the slab path uses, on the
+// calling box: communicator from a unique id, a grouped send / recv pair (to
+// self, standing in for the neighbour exchange of a halo plane) and the
+// in-place all-gather of per-plane sums, all captured into a CUDA graph in
+// relaxed mode on a side stream forked from the capture stream, replayed
+// twice, results checked.  It cannot show that two ranks agree (one GPU), but
+// it fails if the library, its linkage or stream capture of NCCL work is broken.
+int pn_nccl_selftest(int device, int n) {
+    PN_CUDA(cudaSetDevice(device));
+    if (n < 1) { set_error("pn_nccl_selftest: n < 1"); return PN_ERR_INVALID; }
+    ncclUniqueId id;
+    PN_NCCL(ncclGetUniqueId(&id));
+    ncclComm_t comm;
+    PN_NCCL(ncclCommInitRank(&comm, 1, id, 0));
+    double *src = nullptr, *dst = nullptr, *sums = nullptr;
+    cudaStream_t s = nullptr, side = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    int rc = PN_OK;
+    std::vector<double> h(n), back(n), hs(4);
+#define ST_CUDA(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess && rc == PN_OK) { set_error(std::string("pn_nccl_selftest: ") + cudaGetErrorString(e_)); rc = PN_ERR_CUDA; } } while (0)
+#define ST_NCCL(x) do { ncclResult_t r_ = (x); if (r_ != ncclSuccess && rc == PN_OK) { set_error(std::string("pn_nccl_selftest: ") + ncclGetErrorString(r_)); rc = PN_ERR_NCCL; } } while (0)
+    for (int i = 0; i < n; ++i) h[i] = 1.0 + 0.5 * i;
+    ST_CUDA(cudaMalloc(&src, n * sizeof(double)));
+    ST_CUDA(cudaMalloc(&dst, n * sizeof(double)));
+    ST_CUDA(cudaMalloc(&sums, 4 * sizeof(double)));
+    ST_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    ST_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+    ST_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+    ST_CUDA(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
+    if (rc == PN_OK) {
+        ST_CUDA(cudaMemcpy(src, h.data(), n * sizeof(double), cudaMemcpyHostToDevice));
+        ST_CUDA(cudaMemset(dst, 0, n * sizeof(double)));
+        const double four[4] = {3.0, 5.0, 7.0, 11.0};
+        ST_CUDA(cudaMemcpy(sums, four, sizeof(four), cudaMemcpyHostToDevice));
+        ST_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
+        ST_CUDA(cudaEventRecord(fork, s));
+        ST_CUDA(cudaStreamWaitEvent(side, fork, 0));
+        ST_NCCL(ncclGroupStart());
+        ST_NCCL(ncclSend(src, n, ncclDouble, 0, comm, side));
+        ST_NCCL(ncclRecv(dst, n, ncclDouble, 0, comm, side));
+        ST_NCCL(ncclGroupEnd());
+        ST_NCCL(ncclGroupStart());
+        ST_NCCL(ncclAllGather(sums, sums, 4, ncclDouble, comm, side));   // in place, as gather_partials
+        ST_NCCL(ncclGroupEnd());
+        ST_CUDA(cudaEventRecord(join, side));
+        ST_CUDA(cudaStreamWaitEvent(s, join, 0));
+        ST_CUDA(cudaStreamEndCapture(s, &graph));
+        if (rc == PN_OK) ST_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+        for (int rep = 0; rep < 2 && rc == PN_OK; ++rep) ST_CUDA(cudaGraphLaunch(exec, s));
+        ST_CUDA(cudaStreamSynchronize(s));
+        ST_CUDA(cudaMemcpy(back.data(), dst, n * sizeof(double), cudaMemcpyDeviceToHost));
+        ST_CUDA(cudaMemcpy(hs.data(), sums, 4 * sizeof(double), cudaMemcpyDeviceToHost));
+        if (rc == PN_OK && (back != h || hs[0] != 3.0 || hs[1] != 5.0 || hs[2] != 7.0 || hs[3] != 11.0)) {
+            set_error("pn_nccl_selftest: wrong data after send/recv + all-gather");
+            rc = PN_ERR_NCCL;
+        }
+    }
+#undef ST_CUDA
+#undef ST_NCCL
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+    if (fork) cudaEventDestroy(fork);
+    if (join) cudaEventDestroy(join);
+    if (side) cudaStreamDestroy(side);
+    if (s) cudaStreamDestroy(s);
+    cudaFree(src); cudaFree(dst); cudaFree(sums);
+    ncclCommDestroy(comm);
+    return rc;
+}
+
 int pn_create(const pn_desc *d, pn_context **out) {
     if (!d || !out) { set_error("null argument"); return PN_ERR_INVALID; }
     if (d->U < 1 || d->U > 64 || d->nx < 1 || d->ny < 1 || d->nz < 1 || d->nz_local < 1 || d->z0 < 0 ||

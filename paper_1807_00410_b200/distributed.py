@@ -45,6 +45,14 @@ def share_nccl_id(rank, world):
     return buf[0]
 
 
+def nccl_selftest(device=0, n=4096):
+    """One-rank run of the NCCL call patterns of the slab path on this box
+    (communicator, grouped send/recv, in-place all-gather, graph capture on a
+    forked stream); raises on any failure.  pn_nccl_selftest in the C ABI."""
+    from . import _lib
+    _lib.check(_lib.load().pn_nccl_selftest(int(device), int(n)))
+
+
 def make_rank_context(program_or_N, spec, rank, world, device=None, nccl_id=None):
     """Create and fill this rank's slab context.  The fields are the global
     arrays or this rank's planes (spec.z_planes, covering the slab and its

@@ -411,3 +411,48 @@ def test_2d_checkerboard_71_size():
     from paper_1807_00410_b200.problems import make_checkerboard
     from paper_1807_00410_b200.solver import assemble
     assert assemble(tables_2d(1), make_checkerboard()).A.shape[0] == 71 * 71 * 3
+
+
+def test_nccl_call_patterns_on_one_rank():
+    """The NCCL calls of the slab path (communicator from a unique id, grouped
+    send / recv of a plane, in-place all-gather of plane sums) captured into a
+    CUDA graph on a forked stream and replayed, on a one-rank communicator:
+    library, linkage and capture of NCCL work on this box (one GPU cannot show
+    two ranks agreeing; the loopback groups and the gloo tests cover that)."""
+    from paper_1807_00410_b200.distributed import nccl_selftest
+    nccl_selftest(0, 256 * 256 * 4)
+
+
+def test_solve_host_composite_through_the_c_abi():
+    """pn_solve_host (include/pnrte_b200.h): plain host pointers in and out, as
+    a cgo / JNI binding would call it -- no torch tensor crosses the boundary.
+    Faithful solve of a small P3 system == the oracle's bits; fast solve equal
+    to PnContext.solve's."""
+    import ctypes
+    from paper_1807_00410_b200 import _lib
+    from oracle.oracle import StencilOracle
+    N, res = 3, (32, 6, 5)
+    spec = rand_spec(N, res, 515)
+    t = build_tables(N)
+    c = PnContext(t, res, spec.h)
+    c.set_fields(spec)
+    L = _lib.load()
+
+    def run(mode):
+        o = _lib.SolveOpts()
+        o.tol, o.max_iter, o.primal_tol, o.jacobi, o.mode = 1e-8, 600, -1.0, 0, mode
+        o.blas_threads, o.blas_kernel, o.check_every = 8, 0, 0
+        x = np.full(c.R_local, np.nan)
+        hn, hp = np.zeros(600), np.zeros(600)
+        rep = _lib.Report()
+        _lib.check(L.pn_solve_host(c.handle, ctypes.byref(o), x.ctypes.data_as(ctypes.c_void_p), ctypes.byref(rep),
+                                   hn.ctypes.data_as(ctypes.c_void_p), hp.ctypes.data_as(ctypes.c_void_p), 600))
+        return x, rep, hn[:rep.iterations]
+
+    xo, ro = StencilOracle(t, spec).cgnr(tol=1e-8, max_iter=600, blas_threads=8, blas_kernel=0)
+    x, rep, hn = run(1)
+    assert rep.iterations == ro["iterations"] and bool(rep.converged) and x.tobytes() == xo.tobytes()
+    assert hn.tolist() == ro["normal_history"]
+    xf, repf, _ = run(0)
+    xs, rs = c.solve(tol=1e-8, max_iter=600)
+    assert repf.iterations == rs.iterations and xf.tobytes() == xs.cpu().numpy().tobytes()
