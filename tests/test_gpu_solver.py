@@ -428,8 +428,8 @@ def test_solve_host_composite_through_the_c_abi():
     a cgo / JNI binding would call it -- no torch tensor crosses the boundary.
     Faithful solve of a small P3 system == the oracle's bits; fast solve equal
     to PnContext.solve's."""
-    import ctypes
     from paper_1807_00410_b200 import _lib
+    from paper_1807_00410_b200.solver import PnContext
     from oracle.oracle import StencilOracle
     N, res = 3, (32, 6, 5)
     spec = rand_spec(N, res, 515)
