@@ -83,3 +83,14 @@ def test_slab_generation_equals_planes_of_the_grid(idx, n):
                 assert w == v
             else:
                 assert np.ascontiguousarray(np.asarray(v)[:, :, k0:k1]).tobytes() == np.ascontiguousarray(w).tobytes()
+
+
+def test_package_exports_the_reference_solve_path_names():
+    """The package root mirrors the solve-path names of pnrte/__init__.py:17-25
+    (importing does no CUDA work)."""
+    import paper_1807_00410_b200 as pkg
+    for name in ("ProblemSpec", "floor_sigma_t", "make_checkerboard", "SolveReport", "SolutionField", "SparseSystem",
+                 "assemble", "fluence", "reconstruct_radiance", "solve_normal_cg", "unstagger", "solve_pn"):
+        assert hasattr(pkg, name), name
+    f = pkg.SolutionField(staggered=None, collocated=None, unknowns=[(0, 0)], spec=None, report=pkg.SolveReport())
+    assert f.report.iterations == 0 and not f.report.converged
