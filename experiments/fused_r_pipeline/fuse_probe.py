@@ -3,7 +3,7 @@ against the launch chain: bit-identity of fixed-iteration fast solves (solution
 and both histories) on small grids with the bulk path forced, then a config's
 CG iteration time, a sustained fixed-iteration solve and its hashes.
 
-    python tools/fuse_probe.py [--config 4] [--n 0] [--iters 300] [--skip-check]
+    python experiments/fused_r_pipeline/fuse_probe.py  (with the patch applied) [--config 4] [--n 0] [--iters 300] [--skip-check]
 """
 import argparse
 import hashlib

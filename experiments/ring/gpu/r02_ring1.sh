@@ -1,6 +1,6 @@
 mkdir -p gpurun_out
 for v in ring0 ringy; do
-  PNRTE_LIB=variants/$v/libpnrte_b200.so timeout 900 python tools/ring_probe.py > gpurun_out/r02_ring_$v.jsonl 2> gpurun_out/r02_ring_$v.err
+  PNRTE_LIB=variants/$v/libpnrte_b200.so timeout 900 python experiments/ring/ring_probe.py > gpurun_out/r02_ring_$v.jsonl 2> gpurun_out/r02_ring_$v.err
   echo "$v rc=$?"
   cat gpurun_out/r02_ring_$v.jsonl | cut -c1-600
 done

@@ -2,7 +2,7 @@ mkdir -p gpurun_out
 timeout 600 python tools/faithful_probe.py --iters 10 > gpurun_out/r02_faithful_probe.jsonl 2> gpurun_out/r02_faithful_probe.err
 echo "faithful rc=$?"; cat gpurun_out/r02_faithful_probe.jsonl
 for v in ringwgy ringwg0; do
-  PNRTE_LIB=variants/$v/libpnrte_b200.so timeout 600 python tools/ring_probe.py --rings 1 > gpurun_out/r02_ring_$v.jsonl 2> gpurun_out/r02_ring_$v.err
+  PNRTE_LIB=variants/$v/libpnrte_b200.so timeout 600 python experiments/ring/ring_probe.py --rings 1 > gpurun_out/r02_ring_$v.jsonl 2> gpurun_out/r02_ring_$v.err
   echo "$v rc=$?"
   tail -n 1 gpurun_out/r02_ring_$v.jsonl | cut -c1-700
 done

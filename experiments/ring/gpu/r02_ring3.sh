@@ -1,6 +1,6 @@
 mkdir -p gpurun_out
 for v in ringy ring0; do
-  PNRTE_LIB=variants/$v/libpnrte_b200.so timeout 600 python tools/ring_probe.py --rings 1 > gpurun_out/r02_ring3_$v.jsonl 2> gpurun_out/r02_ring3_$v.err
+  PNRTE_LIB=variants/$v/libpnrte_b200.so timeout 600 python experiments/ring/ring_probe.py --rings 1 > gpurun_out/r02_ring3_$v.jsonl 2> gpurun_out/r02_ring3_$v.err
   echo "$v rc=$?"
   grep -c '"same": true' gpurun_out/r02_ring3_$v.jsonl; grep '"same": false' gpurun_out/r02_ring3_$v.jsonl
   tail -n 1 gpurun_out/r02_ring3_$v.jsonl | cut -c1-700

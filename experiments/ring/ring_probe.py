@@ -3,7 +3,7 @@ in one library build: bit-identity of applies and fixed-iteration fast solves on
 small grids (bulk path forced), then config-4 (or --config) apply timings on
 dense / zero operands, burst and sustained with NVML clocks, and the CG iteration.
 
-    python tools/ring_probe.py [--config 4] [--n 256] [--skip-check]
+    python experiments/ring/ring_probe.py  (with the patch applied) [--config 4] [--n 256] [--skip-check]
 """
 import argparse
 import hashlib
