@@ -24,6 +24,8 @@ ap.add_argument("--config", type=int, default=4)
 ap.add_argument("--n", type=int, default=0)
 ap.add_argument("--out", default="gpurun_out/r02_cfg4_solve_parity.json")
 ap.add_argument("--skip-delta", action="store_true")
+ap.add_argument("--skip-fast", action="store_true")
+ap.add_argument("--alts", default="8:2", help="comma list of threads:kernel dot orders for the delta probes")
 a = ap.parse_args()
 
 
@@ -53,12 +55,14 @@ def dump():
     print(json.dumps({k: v for k, v in out.items() if not k.endswith("history")}), flush=True)
 
 
-t0 = time.perf_counter()
-xf, rf = c.solve(tol=cfg.tol, max_iter=cfg.max_iter, mode="fast")
-torch.cuda.synchronize()
-out["fast"] = {"iterations": rf.iterations, "converged": rf.converged, "normal_residual": rf.normal_residual,
-               "seconds": time.perf_counter() - t0, "x_sha256": sha(xf)}
-dump()
+xf = rf = None
+if not a.skip_fast:
+    t0 = time.perf_counter()
+    xf, rf = c.solve(tol=cfg.tol, max_iter=cfg.max_iter, mode="fast")
+    torch.cuda.synchronize()
+    out["fast"] = {"iterations": rf.iterations, "converged": rf.converged, "normal_residual": rf.normal_residual,
+                   "seconds": time.perf_counter() - t0, "x_sha256": sha(xf)}
+    dump()
 t0 = time.perf_counter()
 xs, rs = c.solve(tol=cfg.tol, max_iter=cfg.max_iter, mode="faithful", blas_threads=8, blas_kernel=0)
 torch.cuda.synchronize()
@@ -66,22 +70,31 @@ out["faithful_skx8"] = {"iterations": rs.iterations, "converged": rs.converged, 
                         "seconds": time.perf_counter() - t0, "x_sha256": sha(xs),
                         "normal_history_sha256": hashlib.sha256(np.array(rs.normal_history).tobytes()).hexdigest(),
                         "primal_history_sha256": hashlib.sha256(np.array(rs.primal_history).tobytes()).hexdigest()}
-nf, ns = np.array(rf.normal_history), np.array(rs.normal_history)
-k = min(len(nf), len(ns))
-out["fast_vs_faithful"] = {"iteration_difference": rf.iterations - rs.iterations, "field_rel_l2": rel(xf, xs),
-                           "normal_history_first10_max_rel": float(np.max(np.abs(nf[:10] / ns[:10] - 1))),
-                           "normal_history_max_rel": float(np.max(np.abs(nf[:k] / ns[:k] - 1)))}
+if xf is not None:
+    nf, ns = np.array(rf.normal_history), np.array(rs.normal_history)
+    k = min(len(nf), len(ns))
+    out["fast_vs_faithful"] = {"iteration_difference": rf.iterations - rs.iterations, "field_rel_l2": rel(xf, xs),
+                               "normal_history_first10_max_rel": float(np.max(np.abs(nf[:10] / ns[:10] - 1))),
+                               "normal_history_max_rel": float(np.max(np.abs(nf[:k] / ns[:k] - 1)))}
 out["faithful_normal_history"] = rs.normal_history
 dump()
 del xf
 if not a.skip_delta:
-    t0 = time.perf_counter()
-    xa, ra = c.solve(tol=cfg.tol, max_iter=cfg.max_iter, mode="faithful", blas_threads=8, blas_kernel=2)
-    torch.cuda.synchronize()
-    out["faithful_pairwise8"] = {"iterations": ra.iterations, "seconds": time.perf_counter() - t0,
-                                 "delta_field_rel_l2": rel(xa, xs)}
-    d = out["faithful_pairwise8"]["delta_field_rel_l2"]
-    out["verdict"] = {"iterations_within_1": abs(out["fast_vs_faithful"]["iteration_difference"]) <= 1,
-                      "field_bound": max(1e-8, 4 * d),
-                      "field_within_bound": out["fast_vs_faithful"]["field_rel_l2"] <= max(1e-8, 4 * d)}
-    dump()
+    deltas = {}
+    for spec_ in a.alts.split(","):
+        T, kn = (int(v) for v in spec_.split(":"))
+        t0 = time.perf_counter()
+        xa, ra = c.solve(tol=cfg.tol, max_iter=cfg.max_iter, mode="faithful", blas_threads=T, blas_kernel=kn)
+        torch.cuda.synchronize()
+        name = {0: "skylakex", 1: "haswell", 2: "pairwise"}[kn] + f"_x{T}"
+        deltas[name] = rel(xa, xs)
+        out["faithful_" + name] = {"iterations": ra.iterations, "seconds": time.perf_counter() - t0,
+                                   "delta_field_rel_l2": deltas[name]}
+        del xa
+        dump()
+    if "fast_vs_faithful" in out:
+        d = max(deltas.values())
+        out["verdict"] = {"iterations_within_1": abs(out["fast_vs_faithful"]["iteration_difference"]) <= 1,
+                          "delta_max": d, "field_bound": max(1e-8, 4 * d),
+                          "field_within_bound": out["fast_vs_faithful"]["field_rel_l2"] <= max(1e-8, 4 * d)}
+        dump()
