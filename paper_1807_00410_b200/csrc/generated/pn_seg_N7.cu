@@ -4,4 +4,7 @@ namespace pn {
 template int seg_launch<7>(const SegParams &, const SegGeo &, int, int, bool, const double *, double *,
                             const double *, double *, const double *, const double *, double *, long long, int,
                             const State *, cudaStream_t);
+template int seg_launch_fused_r<7>(const SegParams &, const SegGeo &, const FuseSched &, bool, double *, const double *,
+                                    double *, const double *, double *, const double *, const double *, double *,
+                                    long long, int, const State *, cudaStream_t);
 }

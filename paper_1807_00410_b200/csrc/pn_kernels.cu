@@ -22,6 +22,7 @@
 #include <cooperative_groups.h>
 
 #include "pn_internal.cuh"
+#include "pn_vec.cuh"
 #include "pn_seg_types.cuh"
 
 namespace pn {
@@ -196,31 +197,6 @@ int launch_setup(pn_context *c, bool want_diag, bool want_rhs, cudaStream_t s, d
 __constant__ int c_dx[7] = {0, -1, 1, 0, 0, 0, 0};
 __constant__ int c_dy[7] = {0, 0, 0, -1, 1, 0, 0};
 __constant__ int c_dz[7] = {0, 0, 0, 0, 0, -1, 1};
-
-// Block reduction of up to 3 per-thread values into partials (fixed tree).
-template <int NV>
-__device__ __forceinline__ void block_partials(double (&v)[NV], double *partials, const int *slots, long long slot_stride,
-                                               long long idx) {
-    __shared__ double red[NV][32];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
-#pragma unroll
-    for (int q = 0; q < NV; ++q) {
-        double a = v[q];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) a = __dadd_rn(a, __shfl_down_sync(0xffffffffu, a, o));
-        if (lane == 0) red[q][wid] = a;
-    }
-    __syncthreads();
-    if (wid == 0) {
-#pragma unroll
-        for (int q = 0; q < NV; ++q) {
-            double a = lane < nw ? red[q][lane] : 0.0;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) a = __dadd_rn(a, __shfl_down_sync(0xffffffffu, a, o));
-            if (lane == 0) partials[slots[q] * slot_stride + idx] = a;
-        }
-    }
-}
 
 // red: 0 none, 1 = sum y^2 -> slot 0, 2 = z/zt: sum z*zt -> slot 2, sum z^2 -> slot 1
 // faithful: sequential mul-then-add in table order starting from 0 (scipy
@@ -440,51 +416,8 @@ __global__ void __launch_bounds__(256) k_vec(int op, Geo g, double *y, const dou
 __global__ void __launch_bounds__(256) k_r(Geo g, double *__restrict__ r, const double *__restrict__ w,
                                            const State *st, double *partials, long long slot_stride, int rb, int pst) {
     if (stopped(st)) return;
-    const int kl = blockIdx.y;
-    const long long chunk = (g.plane + rb - 1) / rb;
-    const long long r0 = (long long)blockIdx.x * chunk;
-    const long long r1 = min(g.plane, r0 + chunk);
-    const long long base = (long long)kl * g.plane;
-    const double alpha = st->alpha;
-    double acc = 0.0;
-    long long i0 = base + r0, i1 = base + r1;
-#ifndef PN_VEC_SCALAR
-    // paired (16 B) accesses when every z-plane starts 16 B-aligned (even plane
-    // length, aligned buffers): the element-to-thread map then depends on the
-    // plane-local index only, so the partial sums do not depend on the slab
-    // decomposition.  A leading odd element is done first.
-    const bool paired = !(g.plane & 1) && !((reinterpret_cast<uintptr_t>(r) | reinterpret_cast<uintptr_t>(w)) & 15);
-    if (paired && (i0 & 1) && i0 < i1) {
-        if (threadIdx.x == 0) {
-            const double rv = fma(-alpha, w[i0], r[i0]);
-            r[i0] = rv;
-            acc = fma(rv, rv, acc);
-        }
-        ++i0;
-    }
-    const long long np = paired ? (i1 - i0) >> 1 : 0;
-    double2 *r2 = reinterpret_cast<double2 *>(r + i0);
-    const double2 *w2 = reinterpret_cast<const double2 *>(w + i0);
-#pragma unroll 4
-    for (long long q = threadIdx.x; q < np; q += blockDim.x) {
-        const double2 wv = w2[q];
-        double2 rv = r2[q];
-        rv.x = fma(-alpha, wv.x, rv.x);
-        rv.y = fma(-alpha, wv.y, rv.y);
-        r2[q] = rv;
-        acc = fma(rv.x, rv.x, acc);
-        acc = fma(rv.y, rv.y, acc);
-    }
-    i0 += 2 * np;
-#endif
-    for (long long i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
-        const double rv = fma(-alpha, w[i], r[i]);
-        r[i] = rv;
-        acc = fma(rv, rv, acc);
-    }
-    double v[1] = {acc};
-    const int sl[1] = {3};
-    block_partials<1>(v, partials, sl, slot_stride, (long long)(g.z0 + kl) * pst + blockIdx.x);
+    r_update_block<false>(g.plane, (g.plane + rb - 1) / rb, (int)blockIdx.x, (int)blockIdx.y, g.z0, r, w, st->alpha,
+                          partials, slot_stride, pst);
 }
 
 // fast x += alpha p_old ; p = zt + beta p_old (p only while not stopped).

@@ -805,8 +805,14 @@ static int iteration(std::vector<pn_context *> &cs, const pn_solve_opts *o, bool
         const int cnt = apply_red_count(c, seg, 0);
         PN_TRY(group_apply(cs, 0, 0, &pn_context::p, &pn_context::w, 1, false, true, s, seg, false));
         PN_TRY(launch_plane_sums_scalar(c, 1, cnt, 0, S_ALPHA, s));
-        PN_TRY(launch_r_update(c, s));
-        PN_TRY(group_apply(cs, 1, 0, &pn_context::r, &pn_context::z, 2, jacobi, true, s, seg, false));
+        if (seg && pn_seg_fused_r_ok(c)) {
+            // r -= alpha w and z = A^T r in one launch (same arithmetic and partial slots)
+            PN_TRY(pn_seg_apply_fused_r(c, c->r.p, c->w.p, c->z.p, jacobi ? c->minv.p : nullptr,
+                                        jacobi ? c->zt.p : nullptr, s));
+        } else {
+            PN_TRY(launch_r_update(c, s));
+            PN_TRY(group_apply(cs, 1, 0, &pn_context::r, &pn_context::z, 2, jacobi, true, s, seg, false));
+        }
         PN_TRY(launch_plane_sums_scalar(c, 2 | 4 | 8, cnt, c->vec_bx, S_BETA, s));
         PN_TRY(launch_xp_update(c, (c->*ZT).p, s));
         return PN_OK;

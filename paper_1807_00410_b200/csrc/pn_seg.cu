@@ -20,6 +20,8 @@ struct SegCtx {
     bool ok = false;
     double *sig_pad = nullptr;                // padded sigma_t / sigma_s slabs (nx % 32 != 0)
     size_t sig_pad_n = 0;                     // doubles per field
+    FuseSched fr{};                           // fused residual update + A^T apply
+    bool fr_ok = false;
 };
 
 static bool seg_padded(const pn_context *c) { return c->g.nx % 32 != 0; }
@@ -79,6 +81,67 @@ static bool seg_structure_ok(const pn_context *c) {
 }
 
 bool pn_seg_ok(const pn_context *c) { return c->seg && ((SegCtx *)c->seg)->ok; }
+bool pn_seg_fused_r_ok(const pn_context *c) { return pn_seg_ok(c) && ((SegCtx *)c->seg)->fr_ok; }
+
+// Ticket schedule of k_seg_fr (pn_seg_types.cuh FuseSched).  Single slab, bulk
+// path, orders whose CTAs have the 256 threads the residual update is blocked
+// for; PNRTE_SEG_FUSE_R=0/1 forces.
+static int seg_fuse_prepare(pn_context *c, SegCtx *sc, cudaStream_t s) {
+    sc->fr_ok = false;
+    const SegGeo &g = sc->g;
+    const int rows = seg_rows(c->N), threads = 32 * rows * (seg_pair(c->N) ? 2 : 1);
+    // default for P7 (measured: config 4, 17.13 -> 16.61 ms per iteration, time to 1e-6 68.5 -> 66.5 s,
+    // same bits); the other orders' chunks are smaller than the register path of the embedded
+    // update and stay on the launch chain unless forced
+    bool want = false;
+    if (const char *e = getenv("PNRTE_SEG_FUSE_R")) want = atoi(e) != 0;
+    if (!want || !g.bulk || threads != 256 || c->world > 1 || g.nz < 3 || c->vec_bx < 1) return PN_OK;
+    const int ntiles = (g.nyb + g.tyb - 1) / g.tyb;
+    if (ntiles > FUSE_MAX_TILES) return PN_OK;
+    FuseSched &f = sc->fr;
+    unsigned *ctl = f.ctl, *flags = f.flags;
+    const size_t nflags = (size_t)g.nz * c->vec_bx;
+    // counter and flags start together: epoch 1 over all-zero flags (a re-set field comes
+    // through here again with the epoch advanced, so both are rewound, not only the flags)
+    if (!ctl) PN_CUDA(cudaMalloc(&ctl, 4 * sizeof(unsigned)));
+    if (flags) cudaFree(flags);
+    flags = nullptr;
+    PN_CUDA(cudaMalloc(&flags, nflags * sizeof(unsigned)));
+    const unsigned init[4] = {0u, 1u, 0u, 0u};   // 64-bit counter: ticket (low word), epoch (high word)
+    PN_CUDA(cudaMemcpyAsync(ctl, init, sizeof(init), cudaMemcpyHostToDevice, s));
+    PN_CUDA(cudaMemsetAsync(flags, 0, nflags * sizeof(unsigned), s));
+    PN_CUDA(cudaStreamSynchronize(s));   // setup time; the solve may run on another stream
+    f = FuseSched{};
+    f.ctl = ctl;
+    f.flags = flags;
+    f.ntiles = ntiles;
+    // planes the residual update runs ahead of the apply: far enough that an apply
+    // unit's chunks were drawn more than a device-full of CTAs earlier
+    f.D = 4;
+    if (const char *e = getenv("PNRTE_SEG_FUSE_D")) f.D = std::max(2, atoi(e));
+    if (f.D > g.nz - 1) f.D = g.nz - 1;
+    f.vec_bx = c->vec_bx;
+    f.chunk = (g.plane + c->vec_bx - 1) / c->vec_bx;
+    const long long rowlen = (long long)c->U * 32;
+    unsigned long long t = 0;
+    int c_prev = -1;
+    for (int T = 0; T < ntiles; ++T) {
+        const int jb0 = T * g.tyb, jb1 = std::min(g.nyb, jb0 + g.tyb);
+        const int j_halo = std::min(jb1 * rows, g.ny - 1);   // one row line beyond the tile
+        long long c_hi = (((long long)j_halo + 1) * g.nseg * rowlen - 1) / f.chunk;
+        if (T == ntiles - 1 || c_hi > c->vec_bx - 1) c_hi = c->vec_bx - 1;
+        f.tile_start[T] = (unsigned)t;
+        f.c_lo[T] = c_prev + 1;
+        f.n_u[T] = (int)(c_hi - c_prev);
+        f.n_a[T] = g.nseg * (jb1 - jb0);
+        c_prev = (int)c_hi;
+        t += (unsigned long long)f.D * f.n_u[T] + (unsigned long long)g.nz * f.n_a[T];
+    }
+    if (t >= (1ULL << 31)) return PN_OK;
+    f.tile_start[ntiles] = (unsigned)t;
+    sc->fr_ok = true;
+    return PN_OK;
+}
 
 int pn_seg_prepare(pn_context *c, cudaStream_t s) {
     SegCtx *sc = (SegCtx *)c->seg;
@@ -143,6 +206,7 @@ int pn_seg_prepare(pn_context *c, cudaStream_t s) {
     g.bulk = vec_mb > 96.0;
     if (const char *e = getenv("PNRTE_SEG_BULK")) g.bulk = atoi(e) != 0;
     sc->ok = true;
+    PN_TRY(seg_fuse_prepare(c, sc, s));
     return PN_OK;
 }
 
@@ -172,6 +236,35 @@ int pn_seg_apply(pn_context *c, int trans, const double *x, double *y, int red, 
         PN_N(1) PN_N(2) PN_N(3) PN_N(4) PN_N(5) PN_N(6) PN_N(7)
 #undef PN_N
         default: set_error("segmented kernel: unsupported order"); return PN_ERR_UNSUPPORTED;
+    }
+    c->launches++;
+    return rc;
+}
+
+// r -= alpha w ; z = A^T r with the fused reductions, one launch (k_seg_fr)
+int pn_seg_apply_fused_r(pn_context *c, double *r, const double *w, double *z, const double *minv, double *zt,
+                         cudaStream_t s) {
+    SegCtx *sc = (SegCtx *)c->seg;
+    SegGeo g = sc->g;
+    g.kl0 = 0;
+    g.kst = 1;
+    g.npl = c->g.nzl;
+    const long long stride = (long long)c->g.nz * c->red_bx;
+    const double *sig_t = c->f.data[0], *sig_s = c->f.data[1];
+    if (sc->sig_pad) {
+        sig_t = sc->sig_pad;
+        sig_s = sc->sig_pad + sc->sig_pad_n;
+    }
+    int rc;
+    switch (c->N) {
+#define PN_N(n)                                                                                                  \
+    case n:                                                                                                      \
+        rc = seg_launch_fused_r<n>(*sc->pt, g, sc->fr, minv != nullptr, r, w, z, minv, zt, sig_t, sig_s,        \
+                                   c->partials, stride, c->red_bx, c->state, s);                                 \
+        break;
+        PN_N(1) PN_N(2) PN_N(3) PN_N(4) PN_N(5) PN_N(6) PN_N(7)
+#undef PN_N
+        default: set_error("fused kernel: unsupported order"); return PN_ERR_UNSUPPORTED;
     }
     c->launches++;
     return rc;
@@ -233,6 +326,8 @@ void pn_seg_release(pn_context *c) {
     delete sc->pa;
     delete sc->pt;
     if (sc->sig_pad) cudaFree(sc->sig_pad);
+    if (sc->fr.ctl) cudaFree(sc->fr.ctl);
+    if (sc->fr.flags) cudaFree(sc->fr.flags);
     delete sc;
     c->seg = nullptr;
 }

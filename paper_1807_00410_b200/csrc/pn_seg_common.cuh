@@ -22,6 +22,7 @@
 
 #include "pn_internal.cuh"
 #include "pn_seg_types.cuh"
+#include "pn_vec.cuh"
 
 namespace pn {
 
@@ -450,6 +451,255 @@ __global__ void PN_SEG_BOUNDS(N) k_seg(
         seg_compute<N, TRANS, RED, JAC, TMA, PAD>(prm, g, it, xs, X, Y, rw, minv, zt, lane, half, ra);
     }
     seg_partial<N, RED, JAC>(g, it, ra, lane, warp, partials, slot_stride, rb);
+}
+
+// ---------------------------------------------------------------------------
+#ifndef PN_FR_TICKET
+#define PN_FR_TICKET 1   // 1: work units drawn by atomic ticket; 0: the block index is the ticket
+#endif
+// Fused residual update + A^T apply: one launch does r -= alpha w (the k_r
+// blocks, same arithmetic and partial slots) and z = A^T r with the fused
+// reductions (the k_seg row groups), so the apply reads the new r from L2
+// instead of HBM and the streaming update fills the apply's latency gaps.
+// Work units are drawn by ticket in the order of FuseSched; an update unit
+// publishes its chunk with a release store of the launch epoch, an apply unit
+// acquires the chunks its rows, y / z neighbour rows and segment edges lie in.
+// Every unit a CTA can wait for has a smaller ticket, i.e. belongs to a CTA
+// that is already running and never waits itself: no deadlock.
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned *p, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+
+template <int N, bool JAC, bool PAD>
+__global__ void PN_SEG_BOUNDS(N) k_seg_fr(
+    const __grid_constant__ SegParams prm, const __grid_constant__ SegGeo g, const __grid_constant__ FuseSched f,
+    double *__restrict__ R, const double *__restrict__ W, double *__restrict__ Z, const double *__restrict__ minv,
+    double *__restrict__ zt, const double *__restrict__ st, const double *__restrict__ ss,
+    double *__restrict__ partials, long long slot_stride, int rb, const State *state) {
+    extern __shared__ __align__(16) double smem[];
+    static_assert(SegTune<N>::threads == 256, "fused path: the residual update is blocked for 256 threads");
+    constexpr int WPR = SegTune<N>::wpr, ROWS = SegTune<N>::rows;
+    constexpr int SW = (int)(seg_smem_per_warp<N>() / sizeof(double));
+    constexpr long long rowlen = (long long)(N + 1) * (N + 1) * 32;
+    __shared__ unsigned long long s_ticket;
+    if (seg_stopped(state)) return;   // CTA-uniform; no ticket is drawn by a stopped launch
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // one 64-bit counter: launch epoch in the high word, next ticket in the low one.  The CTA
+    // that draws the last ticket rewinds it for the next launch (nobody else touches it again)
+#if PN_FR_TICKET
+    if (threadIdx.x == 0) {
+        const unsigned long long tk = atomicAdd(reinterpret_cast<unsigned long long *>(f.ctl), 1ULL);
+        s_ticket = tk;
+        if ((unsigned)tk == gridDim.x - 1)
+            *reinterpret_cast<volatile unsigned long long *>(f.ctl) = ((tk >> 32) + 1ULL) << 32;
+    }
+    if (threadIdx.x < ROWS) mbar_init(seg_bar<N>(smem + threadIdx.x * SW), 1);
+    __syncthreads();
+    const unsigned t = (unsigned)s_ticket, epoch = (unsigned)(s_ticket >> 32);
+#else
+    // the block index is the ticket (CTAs of a 1-D grid are dispatched in index order);
+    // the host zeroes the flags before every launch, so "published" is simply 1
+    if (threadIdx.x < ROWS) mbar_init(seg_bar<N>(smem + threadIdx.x * SW), 1);
+    __syncthreads();
+    const unsigned t = blockIdx.x, epoch = 1u;
+    (void)s_ticket;
+#endif
+    // ---- decode the ticket.  Per tile: D update-only steps (planes 0..D-1), then nz steps of
+    // nA apply units; the unit of plane k and index i also updates chunk i (and i + nA, for the
+    // few chunks beyond nA) of plane k + D while its own rows are on their way.
+    int T = 0;
+    while (T + 1 < f.ntiles && t >= f.tile_start[T + 1]) ++T;
+    unsigned u = t - f.tile_start[T];
+    const unsigned nU = (unsigned)f.n_u[T], nA = (unsigned)f.n_a[T], D = (unsigned)f.D, nz = (unsigned)g.nz;
+    const unsigned want = 8u * epoch;   // a chunk is published by eight warp-level increments per launch
+    if (u < D * nU) {
+        // ---- update-only unit: chunk c of this plane (k_r block (c, plane))
+        const unsigned plane = u / nU, idx = u - plane * nU;
+        const int c = f.c_lo[T] + (int)idx;
+        r_update_block<true>(g.plane, f.chunk, c, (int)plane, 0, R, W, state->alpha, partials, slot_stride, rb);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            atomicAdd(f.flags + (size_t)plane * f.vec_bx + c, 8u);
+        }
+        return;
+    }
+    u -= D * nU;
+    const unsigned plane = u / nA, idx = u - plane * nA;
+    const unsigned uplane = plane + D;
+    const int rw = warp / WPR, half = warp % WPR;
+    SegItem it;
+    it.seg = (int)(idx % (unsigned)g.nseg);
+    it.jb = T * g.tyb + (int)(idx / (unsigned)g.nseg);
+    it.kl = (int)plane;
+    it.kg = (int)plane;
+    it.j = it.jb * ROWS + rw;
+    if (it.j >= g.ny) it.j = g.ny;
+    it.rowbase = (((long long)it.kl * g.ny + it.j) * g.nseg + it.seg) * rowlen;
+    __shared__ double s_wsum[8];
+    __shared__ long long s_pidx;
+    const int tid = threadIdx.x;
+    // ---- the embedded update, first chunk: the operands of its first half go in flight now and
+    // stay in registers across the flag polling and the staging of the unit's own rows
+    bool did_update = false;
+    int c_first = 0;
+    double2 wv[8], rv[8];
+    double2 *r2 = nullptr;
+    const double2 *w2 = nullptr;
+    unsigned long long pf = 0, pl = 0;
+    if (idx < nU && uplane < nz) {
+        c_first = f.c_lo[T] + (int)idx;
+        const long long r0 = (long long)c_first * f.chunk, r1 = min(g.plane, r0 + f.chunk);
+        const long long i0 = (long long)uplane * g.plane + r0;
+        did_update = !(g.plane & 1) && !(i0 & 1) && (r1 - r0) == 8192 &&
+                     !((reinterpret_cast<uintptr_t>(R) | reinterpret_cast<uintptr_t>(W)) & 15);
+        if (did_update) {
+            pf = l2_policy_evict_first();
+            pl = l2_policy_evict_last();
+            r2 = reinterpret_cast<double2 *>(R + i0);
+            w2 = reinterpret_cast<const double2 *>(W + i0);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) wv[e] = ldv2<true>(w2 + tid + 256 * e, pf);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) rv[e] = ldv2<true>(r2 + tid + 256 * e, pf);
+        }
+    }
+    // ---- chunks to acquire: threads 0..17 the rows (j0 - 1 .. j0 + ROWS, seg - 1 .. seg + 1) of
+    // this plane, 18 + .. the group's rows of the planes below and above
+    {
+        const int j0 = it.jb * ROWS;
+        int pj = -1, ps = 0, pk = (int)plane;
+        if (tid < 3 * (ROWS + 2)) {
+            pj = j0 - 1 + tid / 3;
+            ps = it.seg - 1 + tid % 3;
+        } else if (tid < 3 * (ROWS + 2) + 2 * ROWS) {
+            const int q = tid - 3 * (ROWS + 2);
+            pj = j0 + q % ROWS;
+            ps = it.seg;
+            pk = (int)plane + (q < ROWS ? -1 : 1);
+        }
+        if (pj >= 0 && pj < g.ny && ps >= 0 && ps < g.nseg && pk >= 0 && pk < g.nz) {
+            const long long off = ((long long)pj * g.nseg + ps) * rowlen;
+            const long long c0 = off / f.chunk, c1 = (off + rowlen - 1) / f.chunk;
+            for (long long c = c0; c <= c1; ++c) {
+                const unsigned *fl = f.flags + (size_t)pk * f.vec_bx + c;
+                while ((int)(ld_acquire_u32(fl) - want) < 0) __nanosleep(64);
+            }
+        }
+    }
+    __syncthreads();
+    asm volatile("fence.proxy.async;\n" ::: "memory");   // the bulk copies read what other SMs just wrote
+    double *xs = smem + rw * SW;
+    if (it.j < g.ny) {
+        seg_stage<N, true>(g, it, xs, R, st, ss, lane, half);
+        cp_async_commit();
+    }
+    // ---- finish the update while the rows land
+    if (did_update) {
+        const double alpha = state->alpha;
+        double acc = 0.0;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            rv[e].x = fma(-alpha, wv[e].x, rv[e].x);
+            rv[e].y = fma(-alpha, wv[e].y, rv[e].y);
+            stv2<true>(r2 + tid + 256 * e, rv[e], pl);
+            acc = fma(rv[e].x, rv[e].x, acc);
+            acc = fma(rv[e].y, rv[e].y, acc);
+        }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) wv[e] = ldv2<true>(w2 + 2048 + tid + 256 * e, pf);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) rv[e] = ldv2<true>(r2 + 2048 + tid + 256 * e, pf);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            rv[e].x = fma(-alpha, wv[e].x, rv[e].x);
+            rv[e].y = fma(-alpha, wv[e].y, rv[e].y);
+            stv2<true>(r2 + 2048 + tid + 256 * e, rv[e], pl);
+            acc = fma(rv[e].x, rv[e].x, acc);
+            acc = fma(rv[e].y, rv[e].y, acc);
+        }
+        // publish per warp (no CTA barrier in front of the apply); the block sum of
+        // ||r||^2 is finished at the end of the unit in block_partials' order
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_down_sync(0xffffffffu, acc, o));
+        __syncwarp();
+        if (lane == 0) {
+            s_wsum[warp] = acc;
+            __threadfence();
+            atomicAdd(f.flags + (size_t)uplane * f.vec_bx + c_first, 1u);
+        }
+        if (tid == 0) s_pidx = (long long)uplane * rb + c_first;
+    }
+    RedAcc ra;
+    if (it.j < g.ny) {
+        cp_async_wait<0>();
+        seg_pair_sync<N>(rw);
+        mbar_wait(seg_bar<N>(xs), 0);
+        if (rw > 0) mbar_wait(seg_bar<N>(xs - SW), 0);
+        if (rw < ROWS - 1 && it.j + 1 < g.ny) mbar_wait(seg_bar<N>(xs + SW), 0);
+        seg_compute<N, 1, 2, JAC, true, PAD>(prm, g, it, xs, R, Z, rw, minv, zt, lane, half, ra);
+    }
+    seg_partial<N, 2, JAC>(g, it, ra, lane, warp, partials, slot_stride, rb);
+    if (did_update) {   // second level of block_partials
+        __syncthreads();
+        if (warp == 0) {
+            double a = lane < 8 ? s_wsum[lane] : 0.0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) a = __dadd_rn(a, __shfl_down_sync(0xffffffffu, a, o));
+            if (lane == 0) partials[3 * slot_stride + s_pidx] = a;
+        }
+    }
+    // chunks the register path did not take: odd sizes, and the few chunks beyond nA (one row line
+    // past the tile); nothing in this tile's remaining steps waits for them sooner than D planes on
+    for (unsigned ci = did_update ? idx + nA : idx; ci < nU && uplane < nz; ci += nA) {
+        const int c = f.c_lo[T] + (int)ci;
+        __syncthreads();
+        r_update_block<true>(g.plane, f.chunk, c, (int)uplane, 0, R, W, state->alpha, partials, slot_stride, rb);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            atomicAdd(f.flags + (size_t)uplane * f.vec_bx + c, 8u);
+        }
+    }
+}
+
+template <int N>
+int seg_launch_fused_r(const SegParams &prm, const SegGeo &g, const FuseSched &f, bool jac, double *r, const double *w,
+                       double *z, const double *minv, double *zt, const double *st, const double *ss,
+                       double *partials, long long slot_stride, int rb, const State *state, cudaStream_t s) {
+    if constexpr (SegTune<N>::threads != 256) {
+        set_error("fused residual update: unsupported order");
+        return PN_ERR_UNSUPPORTED;
+    } else {
+        const size_t smem = SegTune<N>::rows * seg_smem_per_warp<N>();
+        const unsigned nblk = f.tile_start[f.ntiles];
+        int dev = 0;
+        PN_CUDA(cudaGetDevice(&dev));
+#define PN_FR_GO(J, P)                                                                                         \
+    do {                                                                                                       \
+        static std::atomic<unsigned long long> cfg_mask{0};                                                    \
+        const unsigned long long bit_ = 1ULL << (dev & 63);                                                    \
+        if (!(cfg_mask.load() & bit_)) {                                                                       \
+            PN_CUDA(cudaFuncSetAttribute(k_seg_fr<N, J, P>, cudaFuncAttributeMaxDynamicSharedMemorySize,       \
+                                         (int)smem));                                                          \
+            cfg_mask.fetch_or(bit_);                                                                           \
+        }                                                                                                      \
+        if (!PN_FR_TICKET) PN_CUDA(cudaMemsetAsync(f.flags, 0, (size_t)g.nz * f.vec_bx * sizeof(unsigned), s));        \
+        k_seg_fr<N, J, P><<<nblk, 256, smem, s>>>(prm, g, f, r, w, z, minv, zt, st, ss, partials, slot_stride, \
+                                                  rb, state);                                                  \
+    } while (0)
+        const bool pad = g.sx != g.nx;
+        if (jac) { if (pad) PN_FR_GO(true, true); else PN_FR_GO(true, false); }
+        else { if (pad) PN_FR_GO(false, true); else PN_FR_GO(false, false); }
+#undef PN_FR_GO
+        PN_CUDA(cudaGetLastError());
+        return PN_OK;
+    }
 }
 
 template <int N>

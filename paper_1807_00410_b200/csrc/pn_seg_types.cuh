@@ -55,11 +55,31 @@ struct SegGeo {
     FastDiv dseg, dtyb, dnpl;   // set per launch by seg_launch (nseg, min(tyb, nyb), npl)
 };
 
+// Schedule of the fused residual update + A^T apply (k_seg_fr): work units are
+// handed out by ticket.  Per y-tile T of the z-marching traversal and step s:
+// the residual-update chunks (k_r blocks) of plane s that overlap the tile and
+// one row line beyond it, then the row groups of plane s - D of the tile.
+constexpr int FUSE_MAX_TILES = 64;
+struct FuseSched {
+    int ntiles, D, vec_bx, pad_;
+    long long chunk;                             // doubles per residual-update chunk
+    unsigned tile_start[FUSE_MAX_TILES + 1];     // first ticket of tile T
+    int c_lo[FUSE_MAX_TILES], n_u[FUSE_MAX_TILES], n_a[FUSE_MAX_TILES];
+    unsigned *ctl;                               // {next ticket, CTAs finished, epoch}
+    unsigned *flags;                             // [nz][vec_bx]: epoch of the chunk's last update
+};
+
 struct State;
 
 template <int N>
 int seg_launch(const SegParams &prm, const SegGeo &g, int trans, int red, bool jac, const double *x, double *y,
                const double *minv, double *zt, const double *st, const double *ss, double *partials,
                long long slot_stride, int rb, const State *state, cudaStream_t s);
+
+// fused r -= alpha w ; z = A^T r (+ reductions): single slab, bulk path, 256-thread CTAs
+template <int N>
+int seg_launch_fused_r(const SegParams &prm, const SegGeo &g, const FuseSched &f, bool jac, double *r, const double *w,
+                       double *z, const double *minv, double *zt, const double *st, const double *ss,
+                       double *partials, long long slot_stride, int rb, const State *state, cudaStream_t s);
 
 }  // namespace pn

@@ -456,3 +456,31 @@ def test_solve_host_composite_through_the_c_abi():
     xf, repf, _ = run(0)
     xs, rs = c.solve(tol=1e-8, max_iter=600)
     assert repf.iterations == rs.iterations and xf.tobytes() == xs.cpu().numpy().tobytes()
+
+
+@pytest.mark.parametrize("N,res", [(7, (64, 9, 6)), (7, (64, 70, 9)), (3, (80, 13, 4)), (4, (96, 130, 5)), (1, (64, 9, 6))])
+def test_fused_residual_update_is_bit_identical_to_the_chain(N, res, monkeypatch):
+    """Opt-in k_seg_fr (PNRTE_SEG_FUSE_R=1): r -= alpha w inside the A^T apply launch,
+    handed over through L2 under ticket order and release / acquire flags.  Same
+    arithmetic and partial slots as k_r + k_seg: fixed-iteration solves (with and
+    without Jacobi) and a converged solve give the same solution and histories."""
+    from paper_1807_00410_b200.solver import PnContext
+    monkeypatch.setenv("PNRTE_SEG_BULK", "1")
+    monkeypatch.setenv("PNRTE_SMALL_MAX", "0")
+    spec = rand_spec(N, res, 70 + N)
+    got = []
+    for fuse in ("0", "1"):
+        monkeypatch.setenv("PNRTE_SEG_FUSE_R", fuse)
+        c = PnContext(build_tables(N), res, spec.h)
+        c.set_fields(spec)
+        runs = []
+        for kw in (dict(tol=1e-30, max_iter=40), dict(tol=1e-30, max_iter=40, jacobi=True), dict(tol=1e-7, max_iter=4000)):
+            x, rep = c.solve(**kw)
+            runs.append((x.cpu().numpy().tobytes(), rep.iterations, rep.normal_history, rep.primal_history))
+        # fields set again on the same context (the ticket counter and the chunk flags start over together)
+        c.set_fields(spec)
+        x, rep = c.solve(tol=1e-30, max_iter=40)
+        assert (x.cpu().numpy().tobytes(), rep.iterations, rep.normal_history, rep.primal_history) == runs[0]
+        got.append(runs)
+        del c
+    assert got[0] == got[1]
