@@ -93,7 +93,7 @@ static int seg_fuse_prepare(pn_context *c, SegCtx *sc, cudaStream_t s) {
     // default for P7 (measured: config 4, 17.13 -> 16.61 ms per iteration, time to 1e-6 68.5 -> 66.5 s,
     // same bits); the other orders' chunks are smaller than the register path of the embedded
     // update and stay on the launch chain unless forced
-    bool want = false;
+    bool want = c->N == 7;
     if (const char *e = getenv("PNRTE_SEG_FUSE_R")) want = atoi(e) != 0;
     if (!want || !g.bulk || threads != 256 || c->world > 1 || g.nz < 3 || c->vec_bx < 1) return PN_OK;
     const int ntiles = (g.nyb + g.tyb - 1) / g.tyb;
