@@ -93,7 +93,10 @@ static int seg_fuse_prepare(pn_context *c, SegCtx *sc, cudaStream_t s) {
     // default for P7 (measured: config 4, 17.13 -> 16.61 ms per iteration, time to 1e-6 68.5 -> 66.5 s,
     // same bits); the other orders' chunks are smaller than the register path of the embedded
     // update and stay on the launch chain unless forced
-    bool want = c->N == 7;
+    // (and only where every chunk is four whole P7 rows, the shape the embedded register path takes:
+    // ny a multiple of the rows per CTA; other extents run the slower block update and were not timed)
+    const long long chunk0 = (g.plane + c->vec_bx - 1) / c->vec_bx;
+    bool want = c->N == 7 && chunk0 == 8192 && g.plane % chunk0 == 0;
     if (const char *e = getenv("PNRTE_SEG_FUSE_R")) want = atoi(e) != 0;
     if (!want || !g.bulk || threads != 256 || c->world > 1 || g.nz < 3 || c->vec_bx < 1) return PN_OK;
     const int ntiles = (g.nyb + g.tyb - 1) / g.tyb;
